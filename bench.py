@@ -1,0 +1,477 @@
+#!/usr/bin/env python
+"""Benchmark: ResNet-50 v1.5 int8 conv-layer suite on B200 (tcgen05 kind::i8).
+
+Metric (BASELINE.json): "ResNet-50 int8 conv-layer TOPS & % tcgen05 i8 peak at
+1/2/4/8 B200".  One *step* = one pass of the 23 distinct ResNet-50 v1.5 conv
+shapes (pad materialised, valid conv over NHWC u8 x
+[K,R,S,C] i8 -> i32 accumulate -> fused requant to i8) at the per-GPU batch
+(default 32: configs[2] at N=1; N=8 ranks x 32 = configs[4]'s batch 256).
+Scaling is weak (independent images per rank, no collective on the data
+path).  ops = 2*N*OH*OW*K*C*R*S with the real C (stem C=3).
+
+Timing: W warm-up steps, then K steps, each replaying one CUDA graph of the
+23 layer launches with cudaEventRecordExternal events around every layer
+(per-layer kernel durations come from the same timed replays); L2 is
+flushed (512 MiB memset) between steps outside the timed events; barrier +
+synchronize around the timed region; max over ranks.
+
+`--impl reference` times the reference's own CPU implementation of the path
+(oracle/_ref/libtzc_ref.so: eval_tir with the vdot_16x4 instruction — the
+tensorized body on the reference VM — compiled from /root/reference) on a
+bounded sample of the same suite, with every host thread.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "ResNet-50 int8 conv-layer TOPS & % tcgen05 i8 peak at 1/2/4/8 B200"
+SPEC_I8_TOPS = 4500.0
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--batch", type=int, default=32, help="images per GPU")
+    ap.add_argument("--layers", default="", help="comma list of layer names (default: all 23)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0, help="CPU baseline work budget")
+    ap.add_argument("--layer-table", default="", help="write per-layer timings to this JSON path")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def peaks():
+    p = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "source": "fallback (B200_PROFILING.md)"}
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            m = json.load(f)
+        p = {"hbm_gbs": float(m["hbm_gbs"]), "bf16_tflops": float(m["bf16_tflops"]),
+             "source": "measured (MEASURED_PEAKS.json)"}
+    # kind::i8 issues 2x the MACs of kind::f16 per clock on sm_100: the int8
+    # tensor roofline is twice the measured bf16 GEMM burst.
+    p["i8_tops"] = 2.0 * p["bf16_tflops"]
+    return p
+
+
+# ---------------------------------------------------------------------------
+# clocks (NVML polled during the timed region)
+class ClockSampler:
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+               0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown"}
+
+    def __init__(self, index):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:  # noqa: BLE001
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit:
+                        self.reasons.add(name)
+            except Exception:  # noqa: BLE001
+                pass
+            time.sleep(0.002)
+
+    def __enter__(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv:
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------
+class Cudart:
+    """cudaEventRecordWithFlags(..., cudaEventRecordExternal) so timing events
+    survive CUDA-graph capture (torch's Event.record does not)."""
+
+    def __init__(self):
+        import torch  # noqa: F401  (loads the runtime torch ships)
+        self.L = C.CDLL("libcudart.so.12")
+        self.L.cudaEventCreate.argtypes = [C.POINTER(C.c_void_p)]
+        self.L.cudaEventRecordWithFlags.argtypes = [C.c_void_p, C.c_void_p, C.c_uint]
+        self.L.cudaEventElapsedTime.argtypes = [C.POINTER(C.c_float), C.c_void_p, C.c_void_p]
+
+    def event(self):
+        e = C.c_void_p()
+        assert self.L.cudaEventCreate(C.byref(e)) == 0
+        return e
+
+    def record(self, ev, stream):
+        assert self.L.cudaEventRecordWithFlags(ev, C.c_void_p(stream.cuda_stream), 1) == 0
+
+    def ms(self, a, b):
+        f = C.c_float()
+        assert self.L.cudaEventElapsedTime(C.byref(f), a, b) == 0
+        return f.value
+
+
+def build_suite(torch, dev, batch, names, gen):
+    from paper_2101_08458_b200.workloads import RESNET50_V15, requant_scale
+    layers = [L for L in RESNET50_V15 if not names or L.name in names]
+    bufs = []
+    for L in layers:
+        o = L.out_hw()
+        x = torch.randint(0, 256, (batch, L.h, L.h, L.c), dtype=torch.uint8, device=dev, generator=gen)
+        w = torch.randint(-128, 128, (L.k, L.r, L.r, L.c), dtype=torch.int8, device=dev, generator=gen)
+        out = torch.empty((batch, o, o, L.k), dtype=torch.int8, device=dev)
+        bufs.append({"layer": L, "x": x, "w": w, "out": out, "scale": requant_scale(L.c * L.r * L.r)})
+    return layers, bufs
+
+
+def run_ours(args, rank, world, local):
+    import torch
+    import torch.distributed as dist
+    from paper_2101_08458_b200 import device as D
+    from paper_2101_08458_b200._capi import lib
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    assert lib().tzc_b200_device_ok() == 1, "libtzc_b200: no sm_100 device"
+    names = [s for s in args.layers.split(",") if s]
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(1234 + rank)
+    layers, bufs = build_suite(torch, dev, args.batch, names, gen)
+    ops_step = sum(L.ops(args.batch) for L in layers)
+    bytes_step = sum(L.algo_bytes(args.batch) for L in layers)
+    stream = torch.cuda.Stream(device=dev)
+    flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device=dev)
+    rt = Cudart()
+    evs = [rt.event() for _ in range(len(bufs) + 1)]
+
+    def suite(record):
+        for i, b in enumerate(bufs):
+            if record:
+                rt.record(evs[i], stream)
+            D.conv2d(b["x"], b["w"], b["layer"].stride, epilogue="requant_i8", scale=b["scale"],
+                     out=b["out"], stream=stream)
+        if record:
+            rt.record(evs[len(bufs)], stream)
+
+    # eager warm-up: grows workspaces, sets kernel attributes
+    with torch.cuda.stream(stream):
+        suite(False)
+    torch.cuda.synchronize()
+    # graph A: the timed step (no per-layer events inside);
+    # graph B: the same launches with cudaEventRecordExternal events around
+    # every layer, replayed after the timed region for the per-layer table
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=stream):
+        suite(False)
+    graph_l = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph_l, stream=stream):
+        suite(True)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+    def step():
+        flush.zero_()                      # untimed: evict L2 between steps
+        torch.cuda.synchronize()
+        with torch.cuda.stream(stream):   # replay() launches on the current stream
+            e0.record(stream)
+            graph.replay()
+            e1.record(stream)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1)
+
+    def step_layers():
+        flush.zero_()
+        torch.cuda.synchronize()
+        with torch.cuda.stream(stream):
+            graph_l.replay()
+        torch.cuda.synchronize()
+        return [rt.ms(evs[i], evs[i + 1]) for i in range(len(bufs))]
+
+    for _ in range(args.warmup):
+        step()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    step_ms = []
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            step_ms.append(step())
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    per_layer = [[] for _ in bufs]
+    for _ in range(max(3, min(args.steps, 10))):
+        for i, v in enumerate(step_layers()):
+            per_layer[i].append(v)
+    # graph replays launch exactly the captured kernels; count them eagerly once
+    c0 = D.launch_count()
+    with torch.cuda.stream(stream):
+        suite(False)
+    torch.cuda.synchronize()
+    launches_per_step = D.launch_count() - c0
+    total_ms = sum(step_ms)
+    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = float(t.item())
+    ms_step = total_ms / args.steps
+    value = ops_step * world / (ms_step * 1e-3) / 1e12  # TOPS, whole job
+
+    pk = peaks()
+    layer_rows = []
+    for b, v in zip(bufs, per_layer):
+        L = b["layer"]
+        ms = statistics.median(v)
+        ops = L.ops(args.batch)
+        by = L.algo_bytes(args.batch)
+        roof = min(SPEC_I8_TOPS, ops / by * pk["hbm_gbs"] / 1e3)
+        layer_rows.append({"layer": L.name, "ms": ms, "tops": ops / (ms * 1e-3) / 1e12,
+                           "gbs": by / (ms * 1e-3) / 1e9, "roofline_tops_spec": roof,
+                           "plan": plan_of(D, b)})
+    result = {
+        "metric": METRIC,
+        "value": round(value, 2),
+        "unit": "TOPS",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(ms_step, 4),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "u8xi8->i32 (requant i8 out)",
+        "data": "synthetic (uniform u8 activations / i8 weights, torch.Generator seeded per rank)",
+        "config": {"workload": "resnet50_v1.5_int8_conv_suite (23 distinct shapes, SURVEY.md App. A)",
+                   "batch_per_gpu": args.batch, "global_batch": args.batch * world,
+                   "layers": len(layers), "ops_per_step_per_gpu": ops_step,
+                   "algo_bytes_per_step_per_gpu": bytes_step,
+                   "l2": "flushed (512 MiB memset) between timed steps, outside the timed events",
+                   "parallelism": f"dp{world} (batch-sharded, no collective)"},
+        "pct_of_spec_i8_peak": round(100.0 * value / (SPEC_I8_TOPS * world), 2),
+        "gpu_launches": launches_per_step * args.steps,
+        "clocks": clk.summary(),
+    }
+    kern_ms = sum(statistics.median(v) for v in per_layer)  # per-layer event sum (graph B)
+    achieved = ops_step / (kern_ms * 1e-3) / 1e12
+    result["roofline"] = {
+        "bound": "tensor", "kernel": "conv_tc_kernel (tcgen05 kind::i8, all 23 layers)",
+        "achieved": round(achieved, 2), "peak": round(pk["i8_tops"], 1), "unit": "TFLOP/s",
+        "frac": round(achieved / pk["i8_tops"], 4),
+        "peak_basis": f"2 x bf16 burst, {pk['source']}; spec dense i8 = {SPEC_I8_TOPS}",
+        "frac_of_spec": round(achieved / SPEC_I8_TOPS, 4),
+        "suite_cold_hbm_ceiling_frac_of_spec": round(
+            ops_step / sum(L.ops(args.batch) / r["roofline_tops_spec"] for L, r in zip(layers, layer_rows)) / SPEC_I8_TOPS, 4),
+        "traffic": traffic_from_profiles(),
+    }
+    if not args.no_e2e:
+        result["e2e"] = run_e2e(args, torch, D, bufs, stream, ops_step, world, dist)
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        result["cpu_baseline"] = cpu_baseline(args.cpu_seconds, layers)
+    if args.layer_table and rank == 0:
+        with open(args.layer_table, "w") as f:
+            json.dump(layer_rows, f, indent=1)
+    result["layers"] = [{k: (round(v, 4) if isinstance(v, float) else v) for k, v in r.items() if k != "plan"}
+                        for r in layer_rows]
+    if rank == 0:
+        print(json.dumps(result))
+
+
+def plan_of(D, b):
+    L = b["layer"]
+    d, _ = D.conv_desc(tuple(b["x"].shape), tuple(b["w"].shape), L.stride)
+    try:
+        return D.plan_conv(d)
+    except Exception as e:  # noqa: BLE001
+        return {"error": str(e)}
+
+
+def traffic_from_profiles():
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return json.load(f).get("dram_bytes_per_step")
+    return None
+
+
+def run_e2e(args, torch, D, bufs, stream, ops_step, world, dist):
+    """Same metric through the public C ABI with HOST buffers: every step
+    copies each layer's activations + weights from pinned host memory, runs
+    the fused conv, and reads the int8 result back."""
+    host = []
+    h2d = d2h = 0
+    for b in bufs:
+        hx = b["x"].cpu().pin_memory()
+        hw = b["w"].cpu().pin_memory()
+        ho = torch.empty(b["out"].shape, dtype=torch.int8).pin_memory()
+        host.append((hx, hw, ho))
+        h2d += hx.numel() + hw.numel()
+        d2h += ho.numel()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+    def step():
+        with torch.cuda.stream(stream):
+            for b, (hx, hw, ho) in zip(bufs, host):
+                b["x"].copy_(hx, non_blocking=True)
+                b["w"].copy_(hw, non_blocking=True)
+                D.conv2d(b["x"], b["w"], b["layer"].stride, epilogue="requant_i8", scale=b["scale"],
+                         out=b["out"], stream=stream)
+                ho.copy_(b["out"], non_blocking=True)
+
+    for _ in range(max(1, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    steps = max(3, min(args.steps, 10))
+    e0.record(stream)
+    for _ in range(steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=stream.device)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item()) / steps
+    return {"value": round(ops_step * world / (ms * 1e-3) / 1e12, 3), "unit": "TOPS",
+            "ms_per_step": round(ms, 3), "steps": steps,
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+            "path": "tzc_b200_conv2d_i8 (C ABI) with pinned host buffers, H2D+kernel+D2H per layer"}
+
+
+# ---------------------------------------------------------------------------
+# CPU side: the reference implementation (oracle/_ref), bounded sample
+def cpu_sample_ops(layers, budget_macs):
+    """One image, one output row, K' output channels per layer, sized so the
+    whole sample is ~budget_macs multiply-accumulates."""
+    from paper_2101_08458_b200.workloads import conv2d_nhwc_tdsl
+    per = budget_macs / len(layers)
+    items = []
+    for L in layers:
+        o = L.out_hw()
+        kk = max(16, min(L.k, int(per / (o * L.c * L.r * L.r)) // 16 * 16))
+        text = conv2d_nhwc_tdsl(1, L.r, L.h, L.c, kk, L.r, L.r, L.stride)
+        macs = o * kk * L.c * L.r * L.r
+        items.append((L.name, text, macs, L.c % 4 == 0))
+    return items
+
+
+def run_cpu_sample(items, threads, seed=0):
+    from concurrent.futures import ThreadPoolExecutor
+
+    from oracle.pyoracle import Ref
+    prepared = [(nm, t, macs, tir, Ref.random_inputs(t, seed)) for nm, t, macs, tir in items]
+
+    def one(it):
+        nm, t, macs, tir, ins = it
+        if tir:
+            Ref.eval_tir(t, "vdot_16x4", ins)
+        else:
+            Ref.eval_reference(t, ins)
+        return macs
+
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(threads) as ex:
+        macs = sum(ex.map(one, prepared))
+    dt = time.perf_counter() - t0
+    return macs, dt
+
+
+def cpu_baseline(seconds, layers):
+    threads = os.cpu_count() or 1
+    # ~0.8 MMAC/s per thread for eval_tir
+    items = cpu_sample_ops(layers, seconds * threads * 0.8e6)
+    macs, dt = run_cpu_sample(items, threads)
+    return {"value": round(2 * macs / dt / 1e12, 9), "unit": "TOPS", "cores": threads, "kind": "reference",
+            "seconds": round(dt, 2),
+            "sample": f"1 image x 1 output row x K'<=K channels per layer, {len(items)} layers, "
+                      f"{macs} MAC; eval_tir(vdot_16x4) (eval_reference for the C=3 stem), "
+                      f"oracle/_ref/libtzc_ref.so built from /root/reference"}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    from paper_2101_08458_b200.workloads import RESNET50_V15
+    names = [s for s in args.layers.split(",") if s]
+    layers = [L for L in RESNET50_V15 if not names or L.name in names]
+    threads = os.cpu_count() or 1
+    budget = max(1.0, min(args.cpu_seconds, 150.0 / max(1, args.steps + args.warmup)))
+    items = cpu_sample_ops(layers, budget * threads * 0.8e6)
+    for _ in range(args.warmup):
+        run_cpu_sample(items, threads)
+    tot_macs, tot_s = 0, 0.0
+    for _ in range(args.steps):
+        m, s = run_cpu_sample(items, threads)
+        tot_macs += m
+        tot_s += s
+    value = 2 * tot_macs / tot_s / 1e12
+    res = {"metric": METRIC, "value": round(value, 9), "unit": "TOPS", "impl": "reference", "n_gpus": world,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * tot_s / args.steps, 2),
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+           "dtype": "u8xi8->i32", "data": "synthetic (reference random_inputs, seed 0)",
+           "config": {"workload": "resnet50_v1.5_int8_conv_suite (bounded per-layer slices)",
+                      "batch_per_gpu": args.batch, "layers": len(layers)},
+           "cpu_baseline": {"value": round(value, 9), "unit": "TOPS", "cores": threads, "kind": "reference",
+                            "sample": f"per step: 1 image x 1 output row x K' channels of each of {len(layers)} "
+                                      f"layers ({sum(i[2] for i in items)} MAC); eval_tir(vdot_16x4), "
+                                      "eval_reference for the C=3 stem"},
+           "e2e": {"value": round(value, 9), "unit": "TOPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(res))
+
+
+def main():
+    args = parse()
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl")
+    try:
+        run_ours(args, rank, world, local)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

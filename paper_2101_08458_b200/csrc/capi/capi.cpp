@@ -59,9 +59,10 @@ Status problem_from_conv(const tzc_conv_desc& d, Problem* pb) {
   p.w_stride_tap = d.w_stride_tap;
   p.out = d.out;
   const int e = p.f16 ? 2 : 1;
-  if ((d.w_stride_k * e) % 16 || (p.taps > 1 && (d.w_stride_tap * e) % 16))
+  const bool k7 = ((int64_t)d.c * e) % 64 != 0;  // thin channels: explicit im2col path, no TMA on w
+  if (!k7 && ((d.w_stride_k * e) % 16 || (p.taps > 1 && (d.w_stride_tap * e) % 16)))
     return Status(TZC_E_INJECT, "weight strides must be multiples of 16 bytes (TMA)");
-  if (d.r == 1 && d.s == 1 && d.stride == 1) {
+  if (!k7 && d.r == 1 && d.s == 1 && d.stride == 1) {
     // 1x1 unit-stride conv is a plain GEMM over the pixel rows
     p.a_mode = 0;
     p.a_kdim = d.c;

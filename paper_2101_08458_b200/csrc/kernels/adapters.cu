@@ -80,3 +80,108 @@ Status unblock_kernel(const void* src, void* dst, int k, int c, int r, int s, in
 }
 
 }  // namespace tzcb200
+
+// ---- K7: explicit im2col for thin-channel convs (the C = 3 stem) ---------------
+// A row m = (n, oh, ow) gets K index (r*S + s)*C + c, zero-padded to kp
+// columns (kp a multiple of 64 bytes so the GEMM K block is legal).  The
+// padded columns multiply zero-padded weight columns: the sum is unchanged
+// (the reference's own pad legality argument, rewriter.cpp:175-204).
+namespace tzcdev {
+
+// One thread per output pixel row: copy the R contiguous (S*C)-element runs
+// of its receptive field into a shared-memory row (odd word stride: no bank
+// conflicts), zero the tail, then the block writes its 256 contiguous rows
+// with coalesced 16-byte stores.
+constexpr int kIm2colRows = 128;
+
+template <typename T>
+__global__ void __launch_bounds__(kIm2colRows) im2col_pad_kernel(const T* __restrict__ x, T* __restrict__ a, int64_t M,
+                                                               int Hp, int Wp, int C, int R, int S, int stride, int OH,
+                                                               int OW, int rsc, int kp) {
+  extern __shared__ uint32_t srow[];
+  const int row_words = (kp * (int)sizeof(T)) / 4;  // kp*sizeof(T) is a multiple of 64 bytes
+  const int pitch = row_words | 1;                   // odd pitch: conflict-free
+  const int64_t m0 = (int64_t)blockIdx.x * kIm2colRows;
+  const int t = threadIdx.x;
+  const int64_t m = m0 + t;
+  uint32_t* my = srow + t * pitch;
+  for (int w = 0; w < row_words; ++w) my[w] = 0u;
+  if (m < M) {
+    const int64_t n = m / ((int64_t)OH * OW);
+    const int rem = (int)(m - n * OH * OW);
+    const int oh = rem / OW, ow = rem - oh * OW;
+    T* row = reinterpret_cast<T*>(my);
+    const int seg = S * C;
+    for (int r = 0; r < R; ++r) {
+      const T* src = x + ((n * Hp + (int64_t)oh * stride + r) * Wp + (int64_t)ow * stride) * C;
+      for (int j = 0; j < seg; ++j) row[r * seg + j] = src[j];
+    }
+  }
+  __syncthreads();
+  // coalesced copy-out of [rows, row_words] words
+  const int64_t rows = min((int64_t)kIm2colRows, M - m0);
+  uint4* dst = reinterpret_cast<uint4*>(a + m0 * kp);
+  const int vec_per_row = row_words / 4;
+  for (int i = t; i < rows * vec_per_row; i += kIm2colRows) {
+    const int rr = i / vec_per_row, vv = i - rr * vec_per_row;
+    const uint32_t* s = srow + rr * pitch + vv * 4;
+    dst[i] = make_uint4(s[0], s[1], s[2], s[3]);
+  }
+}
+
+template <typename T>
+__global__ void weight_pad_kernel(const T* __restrict__ w, T* __restrict__ b, int K, int R, int S, int C,
+                                  int64_t wsk, int64_t wst, int kp) {
+  const int64_t total = (int64_t)K * kp;
+  const int rsc = R * S * C;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int k = (int)(i / kp);
+    const int kk = (int)(i - (int64_t)k * kp);
+    T v = T(0);
+    if (kk < rsc) {
+      const int tap = kk / C, c = kk - tap * C;
+      v = w[k * wsk + tap * wst + c];
+    }
+    b[i] = v;
+  }
+}
+
+}  // namespace tzcdev
+
+namespace tzcb200 {
+
+Status im2col_pad(const Problem& pb, const void* x, void* a, int kp, cudaStream_t st) {
+  const int rsc = pb.r * pb.s * pb.c;
+  const int eb = pb.f16 ? 2 : 1;
+  const int pitch = ((kp * eb) / 4) | 1;
+  const size_t smem = (size_t)tzcdev::kIm2colRows * pitch * 4;
+  const int64_t blocks = (pb.m + tzcdev::kIm2colRows - 1) / tzcdev::kIm2colRows;
+  if (smem > 200 * 1024 || blocks > INT32_MAX) return Status(TZC_E_INJECT, "im2col row too wide");
+  if (pb.f16) {
+    cudaFuncSetAttribute(tzcdev::im2col_pad_kernel<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    tzcdev::im2col_pad_kernel<uint16_t><<<(int)blocks, tzcdev::kIm2colRows, smem, st>>>(
+        (const uint16_t*)x, (uint16_t*)a, pb.m, pb.hp, pb.wp, pb.c, pb.r, pb.s, pb.stride, pb.oh, pb.ow, rsc, kp);
+  } else {
+    cudaFuncSetAttribute(tzcdev::im2col_pad_kernel<uint8_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    tzcdev::im2col_pad_kernel<uint8_t><<<(int)blocks, tzcdev::kIm2colRows, smem, st>>>(
+        (const uint8_t*)x, (uint8_t*)a, pb.m, pb.hp, pb.wp, pb.c, pb.r, pb.s, pb.stride, pb.oh, pb.ow, rsc, kp);
+  }
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? Status() : Status(TZC_E_DEVICE, cudaGetErrorString(e));
+}
+
+Status weight_pad(const Problem& pb, const void* w, void* b, int kp, cudaStream_t st) {
+  const int64_t n = (int64_t)pb.ngemm * kp;
+  if (pb.f16)
+    tzcdev::weight_pad_kernel<uint16_t><<<blocks_for(n), 256, 0, st>>>((const uint16_t*)w, (uint16_t*)b, pb.ngemm, pb.r,
+                                                                       pb.s, pb.c, pb.w_stride_k, pb.w_stride_tap, kp);
+  else
+    tzcdev::weight_pad_kernel<uint8_t><<<blocks_for(n), 256, 0, st>>>((const uint8_t*)w, (uint8_t*)b, pb.ngemm, pb.r,
+                                                                      pb.s, pb.c, pb.w_stride_k, pb.w_stride_tap, kp);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? Status() : Status(TZC_E_DEVICE, cudaGetErrorString(e));
+}
+
+}  // namespace tzcb200

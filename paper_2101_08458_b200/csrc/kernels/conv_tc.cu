@@ -11,6 +11,7 @@
 #include <cudaTypedefs.h>
 
 #include <atomic>
+#include <cmath>
 #include <cstdio>
 #include <cstring>
 #include <mutex>
@@ -79,31 +80,72 @@ int num_sms() {
 
 namespace {
 
-template <int BN, int KB, bool F16, int AM, bool BMN>
-Status launch_impl(const ConvKernelParams& p, int grid, cudaStream_t stream) {
+// Launch with programmatic stream serialization (PDL): the kernel's
+// prologue (barrier init, TMEM alloc, descriptor prefetch) overlaps the
+// previous grid's tail; griddepcontrol.wait in the kernel keeps the data
+// dependency.  Captured into CUDA graphs as programmatic edges.
+template <typename Kern>
+cudaError_t launch_pdl(Kern kern, dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
+                       const ConvKernelParams& p) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, p);
+}
+
+template <int BN, int KB, bool F16, int AM, bool BMN, int EPM>
+Status launch_kernel(const ConvKernelParams& p, int grid, cudaStream_t stream) {
   using Cfg = ConvCfg<BN, KB>;
-  auto kern = tzcdev::conv_tc_kernel<BN, KB, F16, AM, BMN>;
+  auto kern = tzcdev::conv_tc_kernel<BN, KB, F16, AM, BMN, EPM>;
   static bool attr_done = false;  // per instantiation
   if (!attr_done) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
     if (e != cudaSuccess) return Status(TZC_E_DEVICE, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
     attr_done = true;
   }
-  ConvKernelParams pk = p;
-  if (p.splits > 1) pk.ep_kind = tzcdev::EP_PARTIAL;  // raw partials; fix-up applies the epilogue
-  kern<<<grid, 256, Cfg::SMEM_BYTES, stream>>>(pk);
+  cudaError_t e = launch_pdl(kern, dim3(grid), dim3(tzcdev::EpiCfg<BN>::THREADS), Cfg::SMEM_BYTES, stream, p);
   g_launches.fetch_add(1, std::memory_order_relaxed);
-  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) return Status(TZC_E_DEVICE, std::string("conv_tc launch: ") + cudaGetErrorString(e));
-  if (p.splits > 1) {
-    int64_t groups = (int64_t)p.M * (p.Ngemm / 16);
-    int blocks = (int)std::min<int64_t>((groups + 255) / 256, 4 * 148);
-    tzcdev::splitk_reduce_kernel<F16><<<blocks, 256, 0, stream>>>(p);
-    g_launches.fetch_add(1, std::memory_order_relaxed);
-    e = cudaGetLastError();
-    if (e != cudaSuccess) return Status(TZC_E_DEVICE, std::string("split-K reduce launch: ") + cudaGetErrorString(e));
-  }
   return Status();
+}
+
+template <bool F16, int EPM>
+Status launch_reduce(const ConvKernelParams& p, cudaStream_t stream) {
+  int64_t groups = (int64_t)p.M * (p.Ngemm / 16);
+  int blocks = (int)std::min<int64_t>((groups + 255) / 256, 4 * 148);
+  cudaError_t e = launch_pdl(tzcdev::splitk_reduce_kernel<F16, EPM>, dim3(blocks), dim3(256), 0, stream, p);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  if (e == cudaSuccess) e = cudaGetLastError();
+  if (e != cudaSuccess) return Status(TZC_E_DEVICE, std::string("split-K reduce launch: ") + cudaGetErrorString(e));
+  return Status();
+}
+
+// Epilogue mode from the requested kind (i8 kernels: raw i32 or requant;
+// f16 kernels: raw f32 or fp16 cast).
+template <int BN, int KB, bool F16, int AM, bool BMN>
+Status launch_impl(const ConvKernelParams& p, int grid, cudaStream_t stream) {
+  const int epm = (p.ep_kind == tzcdev::EP_REQUANT_I8) ? tzcdev::EPM_REQUANT
+                  : (p.ep_kind == tzcdev::EP_CAST_F16) ? tzcdev::EPM_F16
+                                                       : tzcdev::EPM_RAW;
+  constexpr int kAlt = F16 ? tzcdev::EPM_F16 : tzcdev::EPM_REQUANT;
+  if (p.splits > 1) {
+    ConvKernelParams pk = p;
+    pk.ep_kind = tzcdev::EP_PARTIAL;  // raw partials; the fix-up applies the epilogue
+    Status st = launch_kernel<BN, KB, F16, AM, BMN, tzcdev::EPM_RAW>(pk, grid, stream);
+    if (!st.ok()) return st;
+    return epm == tzcdev::EPM_RAW ? launch_reduce<F16, tzcdev::EPM_RAW>(p, stream) : launch_reduce<F16, kAlt>(p, stream);
+  }
+  if (epm == tzcdev::EPM_RAW) return launch_kernel<BN, KB, F16, AM, BMN, tzcdev::EPM_RAW>(p, grid, stream);
+  if ((epm == tzcdev::EPM_F16) != F16) return Status(TZC_E_TYPE, "epilogue kind does not match the profile");
+  return launch_kernel<BN, KB, F16, AM, BMN, kAlt>(p, grid, stream);
 }
 
 using LaunchFn = Status (*)(const ConvKernelParams&, int, cudaStream_t);
@@ -124,7 +166,7 @@ struct Entry {
 const Entry kTable[] = {
     TZC_E_BN(128, 0, 0, 0), TZC_E_BN(64, 0, 0, 0), TZC_E_BN(128, 0, 1, 0), TZC_E_BN(64, 0, 1, 0),
     TZC_E_BN(128, 1, 0, 0), TZC_E_BN(64, 1, 0, 0), TZC_E_BN(128, 1, 1, 0), TZC_E_BN(64, 1, 1, 0),
-    TZC_E_BN(128, 1, 0, 1),
+    TZC_E(64, 128, 1, 0, 1), TZC_E(128, 128, 1, 0, 1),
 };
 
 const Entry* find_entry(int bn, int kb, int f16, int am, int bmn) {
@@ -141,23 +183,24 @@ Status enc_check(CUresult r, const char* what) {
   return Status();
 }
 
-// Split-K workspace, cached per process (grown outside timed loops).
+// Device scratch, cached per process and slot (0: split-K partials,
+// 1: K7 im2col rows, 2: K7 padded weights); grown outside timed loops.
 std::mutex g_ws_mu;
-void* g_ws = nullptr;
-size_t g_ws_bytes = 0;
+void* g_ws[3] = {nullptr, nullptr, nullptr};
+size_t g_ws_bytes[3] = {0, 0, 0};
 int g_forced_splits = 0;
 
-Status workspace(size_t bytes, void** out) {
+Status workspace(int slot, size_t bytes, void** out) {
   std::lock_guard<std::mutex> lk(g_ws_mu);
-  if (bytes > g_ws_bytes) {
-    if (g_ws) cudaFree(g_ws);
-    g_ws = nullptr;
-    g_ws_bytes = 0;
-    cudaError_t e = cudaMalloc(&g_ws, bytes);
-    if (e != cudaSuccess) return Status(TZC_E_DEVICE, std::string("split-K workspace: ") + cudaGetErrorString(e));
-    g_ws_bytes = bytes;
+  if (bytes > g_ws_bytes[slot]) {
+    if (g_ws[slot]) cudaFree(g_ws[slot]);
+    g_ws[slot] = nullptr;
+    g_ws_bytes[slot] = 0;
+    cudaError_t e = cudaMalloc(&g_ws[slot], bytes);
+    if (e != cudaSuccess) return Status(TZC_E_DEVICE, std::string("workspace: ") + cudaGetErrorString(e));
+    g_ws_bytes[slot] = bytes;
   }
-  *out = g_ws;
+  *out = g_ws[slot];
   return Status();
 }
 
@@ -181,20 +224,23 @@ Status plan_problem(const Problem& pb, tzc_plan* plan) {
   if (pb.ngemm % 16 != 0) return Status(TZC_E_INJECT, "output channels must be a multiple of 16");
   const int64_t M = pb.m;
   if (M <= 0 || M > INT32_MAX) return Status(TZC_E_SHAPE, "GEMM M out of range");
+  // Widest N tile that divides the output channels: every extra N tile
+  // re-streams the whole A operand (im2col rows) through L2, which is the
+  // binding resource for these layers (ncu: L2-throughput-bound at BN=64).
   int bn = pb.ngemm % 256 == 0 ? 256 : (pb.ngemm % 128 == 0 ? 128 : 64);
   if (pb.b_kn) bn = pb.ngemm % 128 == 0 ? 128 : 64;  // MN-major path instantiated for 64/128
   const int sms = num_sms();
   const int tiles_m = (int)((M + 127) / 128);
-  // Prefer a narrower N tile when it fills the machine and the wide one does not.
-  while (bn > 64 && (int64_t)tiles_m * ((pb.ngemm + bn - 1) / bn) < sms && !pb.b_kn) bn /= 2;
   const int tiles_n = (pb.ngemm + bn - 1) / bn;
   const int num_kb = (int)(pb.taps * (krow_bytes / kb));
   const int tiles = tiles_m * tiles_n;
   int splits = 1;
   if (g_forced_splits > 0) {
     splits = std::min(g_forced_splits, num_kb);
-  } else if (tiles < sms && num_kb >= 8) {
-    splits = std::min((sms + tiles - 1) / tiles, num_kb / 4);
+  } else if (tiles < sms) {
+    // split the reduction to fill the machine, but keep >= 8 K blocks per
+    // split so the int32 partial round trip stays small next to the MMA work
+    splits = std::min((sms + tiles - 1) / tiles, num_kb / 8);
     if (splits < 2) splits = 1;
   }
   const Entry* ent = find_entry(bn, kb, pb.f16, pb.a_mode, pb.b_kn);
@@ -219,6 +265,27 @@ Status run_problem(const Problem& pb, const void* a, const void* b, const void* 
   if (!device_ok()) return Status(TZC_E_DEVICE, "no usable sm_100 (B200) device");
   Status st = load_driver();
   if (!st.ok()) return st;
+  if (((int64_t)pb.c * (pb.f16 ? 2 : 1)) % 64 != 0 && pb.b_kn == 0) {
+    // K7: channel runs too thin for a TMA/UMMA K block (the C=3 stem).
+    // Materialise zero-padded im2col rows + weights and run them as a GEMM.
+    const int e = pb.f16 ? 2 : 1;
+    const int rsc = pb.r * pb.s * pb.c;
+    const int kp = (int)((((int64_t)rsc * e + 63) / 64) * 64 / e);
+    void* wa = nullptr;
+    void* wb = nullptr;
+    st = workspace(1, (size_t)pb.m * kp * e, &wa);
+    if (st.ok()) st = workspace(2, (size_t)pb.ngemm * kp * e, &wb);
+    if (st.ok()) st = im2col_pad(pb, a, wa, kp, stream);
+    if (st.ok()) st = weight_pad(pb, b, wb, kp, stream);
+    if (!st.ok()) return st;
+    Problem g = pb;
+    g.a_mode = tzcdev::A_TILED;
+    g.n = 1; g.hp = 1; g.wp = (int)pb.m; g.r = g.s = g.stride = 1; g.oh = 1; g.ow = (int)pb.m; g.taps = 1;
+    g.c = kp;
+    g.a_kdim = kp; g.a_rows = pb.m; g.a_row_stride = kp;
+    g.w_stride_k = kp; g.w_stride_tap = kp;
+    return run_problem(g, wa, wb, seed, out, ep, stream);
+  }
   tzc_plan plan;
   st = plan_problem(pb, &plan);
   if (!st.ok()) return st;
@@ -298,8 +365,18 @@ Status run_problem(const Problem& pb, const void* a, const void* b, const void* 
   p.out_stride_blk = pb.out.stride_blk;
   p.ep_kind = ep.kind;
   p.scale = ep.scale;
+  p.pow2_k = -1;
+  // |seed + sum| < 2^24 is guaranteed without a seed when K*255*128 < 2^24
+  // (u8 x i8 products): the requant then needs no RNE24 range check.
+  p.range_check = (seed != nullptr || pb.f16 || (int64_t)pb.c * pb.taps * 255 * 128 >= (1 << 24)) ? 1 : 0;
+  {
+    // exact power-of-two scale 2^-k, k in [0, 126]: integer requant path
+    int ex = 0;
+    const float fr = std::frexp(ep.scale, &ex);  // scale = fr * 2^ex, fr in [0.5, 1)
+    if (fr == 0.5f && ex - 1 <= 0 && ex - 1 >= -24) p.pow2_k = -(ex - 1);
+  }
   if (plan.splits > 1) {
-    st = workspace((size_t)plan.workspace_bytes, &p.partial);
+    st = workspace(0, (size_t)plan.workspace_bytes, &p.partial);
     if (!st.ok()) return st;
   }
   const Entry* ent = find_entry(plan.bn, plan.bk_bytes, pb.f16, pb.a_mode, pb.b_kn);
@@ -307,3 +384,10 @@ Status run_problem(const Problem& pb, const void* a, const void* b, const void* 
 }
 
 }  // namespace tzcb200
+
+#ifdef TZC_TRACE
+extern "C" void tzc_trace_dump(unsigned long long* out) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out, tzcdev::g_trace, sizeof(unsigned long long) * 64);
+}
+#endif

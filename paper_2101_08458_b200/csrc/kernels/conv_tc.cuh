@@ -15,7 +15,7 @@
 //               tiled (C, K_out, tap) or MN-major 2-D for fp16 matmul)
 //   warp 1      MMA issuer (lane 0 issues tcgen05.mma, commits to mbarriers)
 //   warp 2      TMEM allocator
-//   warps 4..7  epilogue: tcgen05.ld -> C-seed wrap-add -> requant / cast ->
+//   warps 4..11 epilogue (2 warps per TMEM lane quarter, each half the columns): tcgen05.ld -> C-seed wrap-add -> requant / cast ->
 //               128-bit global stores in the op's (possibly channel-blocked)
 //               output layout
 // Pipelines: STAGES-deep smem ring (full/empty mbarriers), 2 TMEM
@@ -27,6 +27,22 @@
 #include <cstdint>
 
 #include "ptx.cuh"
+
+// Optional cycle tracing for latency debugging (tools/trace_kernel.cu builds
+// with -DTZC_TRACE); compiles to nothing in the library.
+#ifdef TZC_TRACE
+namespace tzcdev {
+__device__ unsigned long long g_trace[64];
+}
+#define TZC_TRACE_POINT(i)                                               \
+  do {                                                                   \
+    if (blockIdx.x == 0) tzcdev::g_trace[(i)] = clock64();               \
+  } while (0)
+#else
+#define TZC_TRACE_POINT(i) \
+  do {                     \
+  } while (0)
+#endif
 
 namespace tzcdev {
 
@@ -50,6 +66,8 @@ struct alignas(64) ConvKernelParams {
   int32_t out_nb;
   int32_t ep_kind;
   float scale;
+  int32_t pow2_k;       // scale == 2^-pow2_k exactly (>= 0), else -1
+  int32_t range_check;  // 0 when |seed + sum| < 2^24 is guaranteed (no seed, K*255*128 < 2^24)
 };
 
 template <int BN, int KB>
@@ -65,21 +83,34 @@ struct ConvCfg {
 };
 
 // ---- epilogue math (bit-exact restatement of the reference semantics) ----
-// cast<i8>(cast<fp32>(c) * s): vm.cpp:79-84 (float_to_int: NaN->0,
-// saturate to int64, trunc toward zero) then wrap to 8 bits (dtype.cpp:40-48).
-__device__ __forceinline__ uint32_t requant_byte(int32_t c, float s) {
-  float f = __fmul_rn(__int2float_rn(c), s);
-  long long q;
-  if (f != f)
-    q = 0;
-  else if (f >= 9223372036854775808.0f)
-    q = 0x7fffffffffffffffLL;
-  else if (f <= -9223372036854775808.0f)
-    q = (-0x7fffffffffffffffLL - 1);
-  else
-    q = __float2ll_rz(f);
-  return static_cast<uint32_t>(q) & 0xffu;
+// Q = cast<i8>(cast<fp32>(c) * s): cast<fp32> is binary32 RNE, the multiply
+// is one RNE rounding (vm.cpp:154-164), float_to_int truncates toward zero
+// with NaN->0 and int64 saturation (vm.cpp:79-84), then wrap to 8 bits
+// (dtype.cpp:40-48).  Both paths below avoid the 16/clk/SM conversion pipe
+// (I2F/F2I), which would otherwise bound the epilogue of thin-K layers.
+
+// General fp32 scale.  int32 -> fp32 RNE via two exact 16-bit halves and
+// one fused rounding; trunc via a round-toward-zero add of 2^23.
+__device__ __forceinline__ uint32_t requant_general(int32_t c, float s) {
+  const float fhi = __int_as_float(0x4B400000 + (c >> 16)) - 12582912.0f;
+  const float flo = __int_as_float(0x4B000000 | ((uint32_t)c & 0xffffu)) - 8388608.0f;
+  const float f = __fmaf_rn(fhi, 65536.0f, flo);  // == RNE_fp32(c)
+  const float p = __fmul_rn(f, s);
+  const uint32_t b = __float_as_uint(p);
+  const uint32_t e = (b >> 23) & 0xffu;
+  uint32_t m;
+  if (e < 150u) {  // |p| < 2^23
+    m = __float_as_uint(__fadd_rz(fabsf(p), 8388608.0f)) & 0x7fffffu;
+  } else if (e < 190u) {  // 2^23 <= |p| < 2^63: p is integral
+    const uint32_t sh = e - 150u;
+    m = sh < 8u ? (((b & 0x7fffffu) | 0x800000u) << sh) : 0u;
+  } else {  // |p| >= 2^63, inf, NaN
+    if (e == 255u && (b & 0x7fffffu)) return 0u;
+    return (b >> 31) ? 0x00u : 0xffu;  // low byte of INT64_MIN / INT64_MAX
+  }
+  return ((b >> 31) ? 0u - m : m) & 0xffu;
 }
+
 
 __device__ __forceinline__ void st_v4(void* p, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
   asm volatile("st.global.v4.b32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(a), "r"(b), "r"(c), "r"(d)
@@ -93,12 +124,30 @@ __device__ __forceinline__ uint4 ld_v4(const void* p) {
   return r;
 }
 
-// Stores 16 consecutive accumulator columns v[0..16) of row m, column n.
-template <bool kF16>
+// Epilogue modes (kernel template parameter, so each instantiation carries
+// only its own straight-line epilogue: the fused path must stay small enough
+// for the instruction cache — a 38 KB all-modes body cost ~5k cycles per
+// 32-column chunk in I-fetch on the first version).
+enum EpMode : int { EPM_RAW = 0, EPM_REQUANT = 1, EPM_F16 = 2 };
+
+__device__ __forceinline__ int64_t out_offset(const ConvKernelParams& p, int m, int n) {
+  if (p.out_nb == p.Ngemm) return (int64_t)m * p.out_stride_m + n;
+  return (int64_t)(n / p.out_nb) * p.out_stride_blk + (int64_t)m * p.out_stride_m + (n % p.out_nb);
+}
+
+// Branch-free RNE to 24 significant bits of |c| (c != INT_MIN handled: a=2^31).
+__device__ __forceinline__ uint32_t rne24(uint32_t a) {
+  const int d = max(8 - (int)__clz(a), 0);  // bits to drop (0 when a < 2^24)
+  const uint32_t mask = (1u << d) - 1u, half = (1u << d) >> 1;
+  const uint32_t rem = a & mask, base = a >> d;
+  const uint32_t up = (rem > half) | ((rem == half) & (base & 1u) & (d > 0 ? 1u : 0u));
+  return (base + up) << d;
+}
+
+// Epilogue of 16 consecutive accumulator columns v[0..16) of row m, column n.
+template <bool kF16, int kEpm>
 __device__ __forceinline__ void store16(const ConvKernelParams& p, int m, int n, const uint32_t* v) {
-  int64_t off = (p.out_nb == p.Ngemm) ? (int64_t)m * p.out_stride_m + n
-                                      : (int64_t)(n / p.out_nb) * p.out_stride_blk +
-                                            (int64_t)m * p.out_stride_m + (n % p.out_nb);
+  const int64_t off = out_offset(p, m, n);
   uint32_t a[16];
 #pragma unroll
   for (int i = 0; i < 16; ++i) a[i] = v[i];
@@ -120,40 +169,72 @@ __device__ __forceinline__ void store16(const ConvKernelParams& p, int m, int n,
       }
     }
   }
-  switch (p.ep_kind) {
-    case EP_REQUANT_I8: {
-      uint32_t w[4];
+  if constexpr (kEpm == EPM_REQUANT) {
+    uint32_t b[16];
+    if (p.pow2_k >= 0) {
+      // s == 2^-k: q = trunc(RNE24(c) / 2^k).  For |c| < 2^24, RNE24(c) == c
+      // and trunc-division is the signed shift (c + ((c>>31) & (2^k-1))) >> k.
+      const int k = p.pow2_k;  // 0 <= k <= 24 (host)
+      const int32_t neg_mask = -(int32_t)((1u << k) - 1u);
+      uint32_t big = 0;
 #pragma unroll
-      for (int j = 0; j < 4; ++j)
-        w[j] = requant_byte((int32_t)a[4 * j], p.scale) | (requant_byte((int32_t)a[4 * j + 1], p.scale) << 8) |
-               (requant_byte((int32_t)a[4 * j + 2], p.scale) << 16) |
-               (requant_byte((int32_t)a[4 * j + 3], p.scale) << 24);
-      st_v4(static_cast<int8_t*>(p.out) + off, w[0], w[1], w[2], w[3]);
-      break;
-    }
-    case EP_CAST_F16: {
-      uint32_t w[8];
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        __half lo = __float2half_rn(__uint_as_float(a[2 * j]));
-        __half hi = __float2half_rn(__uint_as_float(a[2 * j + 1]));
-        w[j] = (uint32_t)__half_as_ushort(lo) | ((uint32_t)__half_as_ushort(hi) << 16);
+      for (int i = 0; i < 16; ++i) {
+        const int32_t c = (int32_t)a[i];
+        const int32_t sgn = c >> 31;  // 0 or -1
+        if (p.range_check) big |= (uint32_t)(c ^ sgn);  // |c| - (c < 0)
+        // trunc(c / 2^k) = (c + (c<0 ? 2^k-1 : 0)) >> k; the correction as an
+        // IMAD (fma pipe) keeps the ALU pipe, which bounds this loop, free
+        b[i] = (uint32_t)((sgn * neg_mask + c) >> k);
       }
-      uint16_t* o = static_cast<uint16_t*>(p.out) + off;
-      st_v4(o, w[0], w[1], w[2], w[3]);
-      st_v4(o + 8, w[4], w[5], w[6], w[7]);
-      break;
-    }
-    default: {  // EP_I32 / EP_F32: raw 32-bit accumulator image
-      uint32_t* o = static_cast<uint32_t*>(p.out) + off;
+      if (p.range_check && __any_sync(__activemask(), big >= (1u << 24))) {
+        // some |c| >= 2^24: the fp32 cast rounds, use the exact RNE24 form
 #pragma unroll
-      for (int j = 0; j < 4; ++j) st_v4(o + 4 * j, a[4 * j], a[4 * j + 1], a[4 * j + 2], a[4 * j + 3]);
+        for (int i = 0; i < 16; ++i) {
+          const int32_t c = (int32_t)a[i];
+          const uint32_t r = rne24(c < 0 ? 0u - (uint32_t)c : (uint32_t)c);
+          const uint32_t mq = r >> k;
+          b[i] = c < 0 ? 0u - mq : mq;
+        }
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) b[i] = requant_general((int32_t)a[i], p.scale);
     }
+    uint32_t w[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      w[j] = __byte_perm(__byte_perm(b[4 * j], b[4 * j + 1], 0x0040), __byte_perm(b[4 * j + 2], b[4 * j + 3], 0x0040),
+                         0x5410);
+    st_v4(static_cast<int8_t*>(p.out) + off, w[0], w[1], w[2], w[3]);
+  } else if constexpr (kEpm == EPM_F16) {
+    uint32_t w[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      __half2 h = __floats2half2_rn(__uint_as_float(a[2 * j]), __uint_as_float(a[2 * j + 1]));
+      w[j] = *reinterpret_cast<uint32_t*>(&h);
+    }
+    uint16_t* o = static_cast<uint16_t*>(p.out) + off;
+    st_v4(o, w[0], w[1], w[2], w[3]);
+    st_v4(o + 8, w[4], w[5], w[6], w[7]);
+  } else {  // raw 32-bit accumulator image (i32 / f32)
+    uint32_t* o = static_cast<uint32_t*>(p.out) + off;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) st_v4(o + 4 * j, a[4 * j], a[4 * j + 1], a[4 * j + 2], a[4 * j + 3]);
   }
 }
 
-template <int BN, int KB, bool kF16, int kAMode, bool kBMN>
-__global__ void __launch_bounds__(256, 1) conv_tc_kernel(const __grid_constant__ ConvKernelParams p) {
+// 4 non-epilogue warps + EPI_WARPS epilogue warps (4 per TMEM lane quarter
+// when BN >= 128: 4 warps per SMSP hide the tcgen05.ld / STG latency).
+template <int BN>
+struct EpiCfg {
+  static constexpr int WARPS = BN >= 128 ? 16 : 8;
+  static constexpr int GROUPS = WARPS / 4;     // column groups per lane quarter
+  static constexpr int COLS = BN / GROUPS;     // columns per epilogue warp (multiple of 32)
+  static constexpr int THREADS = 128 + 32 * WARPS;
+};
+
+template <int BN, int KB, bool kF16, int kAMode, bool kBMN, int kEpm>
+__global__ void __launch_bounds__(EpiCfg<BN>::THREADS, 1) conv_tc_kernel(const __grid_constant__ ConvKernelParams p) {
   using Cfg = ConvCfg<BN, KB>;
   constexpr int BM = Cfg::BM;
   constexpr int STAGES = Cfg::STAGES;
@@ -173,6 +254,7 @@ __global__ void __launch_bounds__(256, 1) conv_tc_kernel(const __grid_constant__
 
   const uint32_t warp = warp_id();
   const uint32_t lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) TZC_TRACE_POINT(0);
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&p.tmA);
@@ -185,7 +267,7 @@ __global__ void __launch_bounds__(256, 1) conv_tc_kernel(const __grid_constant__
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 4);
+      mbar_init(&tempty[a], EpiCfg<BN>::WARPS);
     }
     fence_barrier_init();
   }
@@ -194,6 +276,11 @@ __global__ void __launch_bounds__(256, 1) conv_tc_kernel(const __grid_constant__
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // prologue done: let the next launch start its own, then wait for the
+  // previous grid's writes before touching global memory
+  pdl_launch_dependents();
+  pdl_wait();
+  if (threadIdx.x == 0) TZC_TRACE_POINT(1);
 
   const int num_units = p.num_tiles * p.splits;
 
@@ -241,6 +328,7 @@ __global__ void __launch_bounds__(256, 1) conv_tc_kernel(const __grid_constant__
             phase ^= 1;
           }
         }
+        TZC_TRACE_POINT(2);
       }
     }
   } else if (warp == 1) {
@@ -259,6 +347,7 @@ __global__ void __launch_bounds__(256, 1) conv_tc_kernel(const __grid_constant__
       for (int kb = kb0; kb < kb1; ++kb) {
         mbar_wait(&full[stage], phase);
         tc_fence_after();
+        if (lane == 0 && kb == kb0) TZC_TRACE_POINT(3);
         if (lane == 0) {
           const uint32_t a_base = smem_u32(sA + stage * Cfg::A_BYTES);
           const uint32_t b_base = smem_u32(sB + stage * Cfg::B_BYTES);
@@ -273,7 +362,10 @@ __global__ void __launch_bounds__(256, 1) conv_tc_kernel(const __grid_constant__
             umma<kF16>(tmem_d, adesc, bdesc, IDESC, (kb > kb0 || k > 0) ? 1u : 0u);
           }
           umma_commit(&empty[stage]);
-          if (kb == kb1 - 1) umma_commit(&tfull[acc]);
+          if (kb == kb1 - 1) {
+            umma_commit(&tfull[acc]);
+            TZC_TRACE_POINT(4);
+          }
         }
         __syncwarp();
         if (++stage == STAGES) {
@@ -288,7 +380,9 @@ __global__ void __launch_bounds__(256, 1) conv_tc_kernel(const __grid_constant__
     }
   } else if (warp >= 4) {
     // ===================== epilogue =====================
-    const uint32_t q = warp & 3;  // TMEM lane quarter this warp may access
+    const uint32_t q = warp & 3;         // TMEM lane quarter this warp may access
+    const uint32_t h = (warp - 4) >> 2;  // column group
+    constexpr int HALF = EpiCfg<BN>::COLS;
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int u = blockIdx.x; u < num_units; u += gridDim.x) {
@@ -297,12 +391,16 @@ __global__ void __launch_bounds__(256, 1) conv_tc_kernel(const __grid_constant__
       const int m = m_tile * BM + q * 32 + lane;
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
+      if (threadIdx.x == 128) TZC_TRACE_POINT(5);
 #pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
+      for (int c = 0; c < HALF / 32; ++c) {
+        const int col = h * HALF + c * 32;
         uint32_t v[32];
-        tmem_ld32(tmem_base + ((q * 32) << 16) + acc * BN + c * 32, v);
+        if (threadIdx.x == 128) TZC_TRACE_POINT(8 + 3 * c);
+        tmem_ld32(tmem_base + ((q * 32) << 16) + acc * BN + col, v);
         tmem_ld_wait();
-        const int n = n_tile * BN + c * 32;
+        if (threadIdx.x == 128) TZC_TRACE_POINT(9 + 3 * c);
+        const int n = n_tile * BN + col;
         if (m < p.M) {
           if (p.ep_kind == EP_PARTIAL) {
             uint32_t* o = static_cast<uint32_t*>(p.partial) + ((int64_t)split * p.M + m) * p.Ngemm + n;
@@ -310,13 +408,15 @@ __global__ void __launch_bounds__(256, 1) conv_tc_kernel(const __grid_constant__
             for (int j = 0; j < 8; ++j)
               if (n + 4 * j < p.Ngemm) st_v4(o + 4 * j, v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
           } else {
-            if (n < p.Ngemm) store16<kF16>(p, m, n, v);
-            if (n + 16 < p.Ngemm) store16<kF16>(p, m, n + 16, v + 16);
+            if (n < p.Ngemm) store16<kF16, kEpm>(p, m, n, v);
+            if (n + 16 < p.Ngemm) store16<kF16, kEpm>(p, m, n + 16, v + 16);
           }
         }
+        if (threadIdx.x == 128) TZC_TRACE_POINT(10 + 3 * c);
       }
       tc_fence_before();
       __syncwarp();
+      if (threadIdx.x == 128) TZC_TRACE_POINT(6);
       if (lane == 0) mbar_arrive(&tempty[acc]);
       if (++acc == 2) {
         acc = 0;
@@ -324,7 +424,9 @@ __global__ void __launch_bounds__(256, 1) conv_tc_kernel(const __grid_constant__
       }
     }
   }
+  __syncwarp();  // roles diverge within warps 0/1; bar.sync requires convergence
   __syncthreads();
+  if (threadIdx.x == 0) TZC_TRACE_POINT(7);
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc<Cfg::TMEM_COLS>(tmem_base);
@@ -335,8 +437,10 @@ __global__ void __launch_bounds__(256, 1) conv_tc_kernel(const __grid_constant__
 // sums are combined with wrapping int32 adds, which is associative, so the
 // result is bit-identical to any reduction order (F8); fp32 partials are
 // combined in split order.
-template <bool kF16>
+template <bool kF16, int kEpm>
 __global__ void splitk_reduce_kernel(const __grid_constant__ ConvKernelParams p) {
+  pdl_launch_dependents();
+  pdl_wait();
   const int64_t groups = (int64_t)p.M * (p.Ngemm / 16);
   for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < groups;
        g += (int64_t)gridDim.x * blockDim.x) {
@@ -363,7 +467,7 @@ __global__ void splitk_reduce_kernel(const __grid_constant__ ConvKernelParams p)
         }
       }
     }
-    store16<kF16>(p, m, n, v);
+    store16<kF16, kEpm>(p, m, n, v);
   }
 }
 

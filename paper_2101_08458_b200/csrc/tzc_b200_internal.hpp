@@ -49,6 +49,9 @@ Status unblock_data(const void* src, void* dst, int c, int h, int w, int cb, int
 Status unblock_kernel(const void* src, void* dst, int k, int c, int r, int s, int kb, int cb, int eb,
                       cudaStream_t st);
 
+Status im2col_pad(const Problem& pb, const void* x, void* a, int kp, cudaStream_t st);
+Status weight_pad(const Problem& pb, const void* w, void* b, int kp, cudaStream_t st);
+
 extern std::atomic<uint64_t> g_launches;
 
 }  // namespace tzcb200

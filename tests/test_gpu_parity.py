@@ -45,7 +45,7 @@ def test_gemm_i8_no_seed(cuda):
     assert np.array_equal(ref, got)
 
 
-@pytest.mark.parametrize("scale", [2.0 ** -14, 2.0 ** -7, 0.0123])
+@pytest.mark.parametrize("scale", [2.0 ** -14, 2.0 ** -7, 1.0, 2.0 ** -40, 0.0123, -0.37, 3.0e30, 1e-40])
 def test_gemm_i8_requant_bitexact(cuda, scale):
     ref, got = _gemm_case(cuda, 256, 256, 512, epilogue="requant_i8", scale=scale)
     assert np.array_equal(ref, got), f"mismatches: {(ref != got).sum()}"
@@ -67,6 +67,8 @@ CONV_CASES = [
     (1, 14, 14, 256, 512, 1, 2),
     (3, 16, 16, 512, 256, 3, 1),
     (1, 58, 58, 64, 64, 3, 1),
+    (2, 21, 21, 3, 64, 7, 2),     # C=3 stem: K7 im2col path
+    (1, 15, 15, 3, 64, 7, 2),
 ]
 
 
@@ -119,3 +121,24 @@ def test_conv_f16(cuda):
     # the cast is RNE of the fp32 accumulator; compare in value space
     hv = h.view(np.float16).astype(np.float64)
     assert rel_dev(ref, hv) <= 1e-3 + 2 ** -11
+
+
+EDGE_I32 = [0, 1, -1, 127, 128, 255, 256, -128, -129, 2**24 - 1, 2**24, 2**24 + 1, 2**24 + 3,
+            -(2**24) - 1, 2**25 + 2, 2**30 + 2**6, 2**31 - 1, -(2**31), -(2**31) + 1, 16383, -16385,
+            2147483647 - 64, 33554431, -33554431]
+
+
+@pytest.mark.parametrize("scale", [2.0 ** -7, 2.0 ** -14, 1.0, 2.0 ** -31, 2.0 ** -32, 0.0078125, 0.3,
+                                   -1.5, 7.0e20, 9.3e18, -9.3e18, 1e-45, float("inf")])
+def test_requant_edges_bitexact(cuda, scale):
+    """A = 0, so C == C-seed: drives the fused requant over int32 edge values
+    (RNE boundaries at 2^24, INT_MIN/INT_MAX, saturation at 2^63, denormals)."""
+    rng = np.random.default_rng(5)
+    vals = np.array(EDGE_I32 + list(rng.integers(-(2**31), 2**31, size=4096 - len(EDGE_I32))), dtype=np.int64)
+    m, n, k = 128, 32, 64
+    seed = vals[: m * n].astype(np.int32).reshape(m, n)
+    A = np.zeros((m, k), np.uint8)
+    B = Orc.random_tensor("i8", (n, k), 9)
+    got = D.gemm(to_dev(A, cuda), to_dev(B, cuda), to_dev(seed, cuda), epilogue="requant_i8",
+                 scale=scale).cpu().numpy()
+    assert np.array_equal(Orc.requant_i8(seed, scale), got)
