@@ -21,16 +21,18 @@ int report(const Status& st) {
 
 Status check_layout(const tzc_out_layout& o, int ngemm, int64_t m) {
   if (o.nb <= 0 || ngemm % o.nb != 0) return Status(TZC_E_SHAPE, "out layout: nb must divide the channel count");
-  if (!(o.nb == 16 || o.nb % 32 == 0)) return Status(TZC_E_INJECT, "out layout: nb must be 16 or a multiple of 32");
-  if (o.stride_m < o.nb || o.stride_m % 16 != 0) return Status(TZC_E_INJECT, "out layout: stride_m must be >= nb and a multiple of 16");
-  if (o.nb != ngemm && (o.stride_blk < (m - 1) * o.stride_m + o.nb || o.stride_blk % 16 != 0))
-    return Status(TZC_E_INJECT, "out layout: stride_blk must separate channel blocks and be a multiple of 16");
+  if (o.stride_m < o.nb) return Status(TZC_E_SHAPE, "out layout: stride_m must be >= nb");
+  if (o.nb != ngemm && o.stride_blk < (m - 1) * o.stride_m + o.nb)
+    return Status(TZC_E_SHAPE, "out layout: stride_blk must separate channel blocks");
   return Status();
 }
 
-Status check_ptr(const void* p, const char* what, bool nullable) {
+// TMA operands need 16-byte aligned base addresses; outputs / seeds do not
+// (the epilogue falls back to element stores).
+Status check_ptr(const void* p, const char* what, bool nullable, bool tma = true) {
   if (!p) return nullable ? Status() : Status(TZC_E_MISSING_INPUT, std::string(what) + " is NULL");
-  if (reinterpret_cast<uintptr_t>(p) % 16 != 0) return Status(TZC_E_INJECT, std::string(what) + " must be 16-byte aligned");
+  if (tma && reinterpret_cast<uintptr_t>(p) % 16 != 0)
+    return Status(TZC_E_INJECT, std::string(what) + " must be 16-byte aligned (TMA)");
   return Status();
 }
 
@@ -59,7 +61,7 @@ Status problem_from_conv(const tzc_conv_desc& d, Problem* pb) {
   p.w_stride_tap = d.w_stride_tap;
   p.out = d.out;
   const int e = p.f16 ? 2 : 1;
-  const bool k7 = ((int64_t)d.c * e) % 64 != 0;  // thin channels: explicit im2col path, no TMA on w
+  const bool k7 = ((int64_t)d.c * e) % 16 != 0;  // thin channels: explicit im2col path, no TMA on x/w
   if (!k7 && ((d.w_stride_k * e) % 16 || (p.taps > 1 && (d.w_stride_tap * e) % 16)))
     return Status(TZC_E_INJECT, "weight strides must be multiples of 16 bytes (TMA)");
   if (!k7 && d.r == 1 && d.s == 1 && d.stride == 1) {
@@ -98,6 +100,7 @@ Status problem_from_gemm(const tzc_gemm_desc& d, Problem* pb) {
   p.out = d.out;
   const int e = p.f16 ? 2 : 1;
   if ((int64_t)d.k * e % 16) return Status(TZC_E_INJECT, "K row must be a multiple of 16 bytes (TMA)");
+  if (d.b_kn && (int64_t)d.n * e % 16) return Status(TZC_E_INJECT, "[K,N] row must be a multiple of 16 bytes (TMA)");
   Status st = check_layout(d.out, d.n, d.m);
   if (!st.ok()) return st;
   *pb = p;
@@ -128,8 +131,8 @@ int run_conv(const tzc_conv_desc* d, int profile, const void* x, const void* w, 
   Status st = problem_from_conv(*d, &pb);
   if (st.ok()) st = check_ptr(x, "x", false);
   if (st.ok()) st = check_ptr(w, "w", false);
-  if (st.ok()) st = check_ptr(seed, "c_seed", true);
-  if (st.ok()) st = check_ptr(out, "out", false);
+  if (st.ok()) st = check_ptr(seed, "c_seed", true, false);
+  if (st.ok()) st = check_ptr(out, "out", false, false);
   if (!st.ok()) return report(st);
   return report(run_problem(pb, x, w, seed, out, *ep, static_cast<cudaStream_t>(stream)));
 }
@@ -142,8 +145,8 @@ int run_gemm(const tzc_gemm_desc* d, int profile, const void* a, const void* b, 
   Status st = problem_from_gemm(*d, &pb);
   if (st.ok()) st = check_ptr(a, "a", false);
   if (st.ok()) st = check_ptr(b, "b", false);
-  if (st.ok()) st = check_ptr(seed, "c_seed", true);
-  if (st.ok()) st = check_ptr(out, "out", false);
+  if (st.ok()) st = check_ptr(seed, "c_seed", true, false);
+  if (st.ok()) st = check_ptr(out, "out", false, false);
   if (!st.ok()) return report(st);
   return report(run_problem(pb, a, b, seed, out, *ep, static_cast<cudaStream_t>(stream)));
 }

@@ -208,20 +208,47 @@ Status workspace(int slot, size_t bytes, void** out) {
 
 void set_forced_splits(int s) { g_forced_splits = s; }
 
+// ---- K7 (thin-channel) rewrite ------------------------------------------------
+bool needs_k7(const Problem& pb) { return pb.b_kn == 0 && ((int64_t)pb.c * (pb.f16 ? 2 : 1)) % 16 != 0; }
+
+Problem k7_gemm(const Problem& pb, int* kp_out) {
+  const int e = pb.f16 ? 2 : 1;
+  const int rsc = pb.r * pb.s * pb.c;
+  const int kp = (int)((((int64_t)rsc * e + 63) / 64) * 64 / e);  // K padded to 64 bytes
+  Problem g = pb;
+  g.a_mode = tzcdev::A_TILED;
+  g.n = 1;
+  g.hp = 1;
+  g.wp = (int)pb.m;
+  g.r = g.s = g.stride = 1;
+  g.oh = 1;
+  g.ow = (int)pb.m;
+  g.taps = 1;
+  g.c = kp;
+  g.a_kdim = kp;
+  g.a_rows = pb.m;
+  g.a_row_stride = kp;
+  g.w_stride_k = kp;
+  g.w_stride_tap = kp;
+  *kp_out = kp;
+  return g;
+}
+
 // ---- planning ----------------------------------------------------------------
-Status plan_problem(const Problem& pb, tzc_plan* plan) {
+Status plan_problem(const Problem& pb_in, tzc_plan* plan) {
+  int kp = 0;
+  const Problem pb = needs_k7(pb_in) ? k7_gemm(pb_in, &kp) : pb_in;
   const int e = pb.f16 ? 2 : 1;
   const int64_t krow_bytes = (int64_t)pb.c * e;  // contiguous K run per tap
-  int kb;
-  if (krow_bytes % 128 == 0)
-    kb = 128;
-  else if (krow_bytes % 64 == 0)
-    kb = 64;
-  else
+  // K block: one 128-byte (SWIZZLE_128B) or 64-byte (SWIZZLE_64B) smem row.
+  // A ragged last block per tap is zero-filled by TMA out-of-bounds handling
+  // (the channel / K extent is the innermost tensor-map dimension), which is
+  // exact: zero products (the reference's own pad argument, rewriter.cpp:175-204).
+  if (krow_bytes % 16 != 0)
     return Status(TZC_E_INJECT, "reduction run of " + std::to_string(krow_bytes) +
-                                    " bytes is not a multiple of 64 (TMA/UMMA K block); pad channels or use the layout adapter");
-  if (pb.b_kn && kb != 128) return Status(TZC_E_INJECT, "fp16 [K,N] operand needs K*2 % 128 == 0");
-  if (pb.ngemm % 16 != 0) return Status(TZC_E_INJECT, "output channels must be a multiple of 16");
+                                    " bytes is not a multiple of 16 (TMA stride); use the K7 path");
+  int kb = (krow_bytes % 128 == 0) ? 128 : (krow_bytes % 64 == 0) ? 64 : (krow_bytes > 64 ? 128 : 64);
+  if (pb.b_kn) kb = 128;  // MN-major fp16 path is instantiated for 128-byte K blocks
   const int64_t M = pb.m;
   if (M <= 0 || M > INT32_MAX) return Status(TZC_E_SHAPE, "GEMM M out of range");
   // Widest N tile that divides the output channels: every extra N tile
@@ -232,12 +259,12 @@ Status plan_problem(const Problem& pb, tzc_plan* plan) {
   const int sms = num_sms();
   const int tiles_m = (int)((M + 127) / 128);
   const int tiles_n = (pb.ngemm + bn - 1) / bn;
-  const int num_kb = (int)(pb.taps * (krow_bytes / kb));
+  const int num_kb = (int)(pb.taps * ((krow_bytes + kb - 1) / kb));
   const int tiles = tiles_m * tiles_n;
   int splits = 1;
   if (g_forced_splits > 0) {
     splits = std::min(g_forced_splits, num_kb);
-  } else if (tiles < sms) {
+  } else if (tiles < sms && pb.ngemm % 16 == 0) {
     // split the reduction to fill the machine, but keep >= 8 K blocks per
     // split so the int32 partial round trip stays small next to the MMA work
     splits = std::min((sms + tiles - 1) / tiles, num_kb / 8);
@@ -265,12 +292,12 @@ Status run_problem(const Problem& pb, const void* a, const void* b, const void* 
   if (!device_ok()) return Status(TZC_E_DEVICE, "no usable sm_100 (B200) device");
   Status st = load_driver();
   if (!st.ok()) return st;
-  if (((int64_t)pb.c * (pb.f16 ? 2 : 1)) % 64 != 0 && pb.b_kn == 0) {
-    // K7: channel runs too thin for a TMA/UMMA K block (the C=3 stem).
-    // Materialise zero-padded im2col rows + weights and run them as a GEMM.
+  if (needs_k7(pb)) {
+    // K7: channel runs too thin for TMA (the C=3 stem).  Materialise
+    // zero-padded im2col rows + weights and run them as a GEMM.
+    int kp = 0;
+    const Problem g = k7_gemm(pb, &kp);
     const int e = pb.f16 ? 2 : 1;
-    const int rsc = pb.r * pb.s * pb.c;
-    const int kp = (int)((((int64_t)rsc * e + 63) / 64) * 64 / e);
     void* wa = nullptr;
     void* wb = nullptr;
     st = workspace(1, (size_t)pb.m * kp * e, &wa);
@@ -278,12 +305,6 @@ Status run_problem(const Problem& pb, const void* a, const void* b, const void* 
     if (st.ok()) st = im2col_pad(pb, a, wa, kp, stream);
     if (st.ok()) st = weight_pad(pb, b, wb, kp, stream);
     if (!st.ok()) return st;
-    Problem g = pb;
-    g.a_mode = tzcdev::A_TILED;
-    g.n = 1; g.hp = 1; g.wp = (int)pb.m; g.r = g.s = g.stride = 1; g.oh = 1; g.ow = (int)pb.m; g.taps = 1;
-    g.c = kp;
-    g.a_kdim = kp; g.a_rows = pb.m; g.a_row_stride = kp;
-    g.w_stride_k = kp; g.w_stride_tap = kp;
     return run_problem(g, wa, wb, seed, out, ep, stream);
   }
   tzc_plan plan;
@@ -348,7 +369,7 @@ Status run_problem(const Problem& pb, const void* a, const void* b, const void* 
 
   p.M = (int32_t)pb.m;
   p.Ngemm = pb.ngemm;
-  p.c_blocks = (int32_t)((int64_t)pb.c * e / plan.bk_bytes);
+  p.c_blocks = (int32_t)(((int64_t)pb.c * e + plan.bk_bytes - 1) / plan.bk_bytes);
   p.num_kb = p.c_blocks * pb.taps;
   p.S = pb.s;
   p.OW = pb.ow;
@@ -365,6 +386,15 @@ Status run_problem(const Problem& pb, const void* a, const void* b, const void* 
   p.out_stride_blk = pb.out.stride_blk;
   p.ep_kind = ep.kind;
   p.scale = ep.scale;
+  {
+    // vectorised epilogue: every 16-column piece of out / seed starts 16-byte aligned
+    const int eo = (ep.kind == tzcdev::EP_REQUANT_I8) ? 1 : (ep.kind == tzcdev::EP_CAST_F16) ? 2 : 4;
+    auto al = [](int64_t elems, int eb) { return (elems * eb) % 16 == 0; };
+    bool ok = pb.ngemm % 16 == 0 && (pb.out.nb % 16 == 0) && al(pb.out.stride_m, eo) && al(pb.out.stride_blk, eo) &&
+              reinterpret_cast<uintptr_t>(out) % 16 == 0;
+    if (seed) ok = ok && al(pb.out.stride_m, 4) && al(pb.out.stride_blk, 4) && reinterpret_cast<uintptr_t>(seed) % 16 == 0;
+    p.vec_ok = ok ? 1 : 0;
+  }
   p.pow2_k = -1;
   // |seed + sum| < 2^24 is guaranteed without a seed when K*255*128 < 2^24
   // (u8 x i8 products): the requant then needs no RNE24 range check.

@@ -67,6 +67,7 @@ struct alignas(64) ConvKernelParams {
   int32_t ep_kind;
   float scale;
   int32_t pow2_k;       // scale == 2^-pow2_k exactly (>= 0), else -1
+  int32_t vec_ok;       // 16-column output/seed pieces are 16-byte aligned
   int32_t range_check;  // 0 when |seed + sum| < 2^24 is guaranteed (no seed, K*255*128 < 2^24)
 };
 
@@ -148,10 +149,21 @@ __device__ __forceinline__ uint32_t rne24(uint32_t a) {
 template <bool kF16, int kEpm>
 __device__ __forceinline__ void store16(const ConvKernelParams& p, int m, int n, const uint32_t* v) {
   const int64_t off = out_offset(p, m, n);
+  // vector path: 16 columns in range and every piece 16-byte aligned (host
+  // checked); otherwise element-wise (ragged channel counts, odd strides)
+  const bool vec = p.vec_ok && n + 16 <= p.Ngemm;
   uint32_t a[16];
 #pragma unroll
   for (int i = 0; i < 16; ++i) a[i] = v[i];
-  if (p.seed != nullptr) {
+  if (p.seed != nullptr && !vec) {
+    const uint32_t* sd = static_cast<const uint32_t*>(p.seed);
+#pragma unroll 1
+    for (int i = 0; i < 16; ++i) {
+      if (n + i >= p.Ngemm) break;
+      const uint32_t t = sd[out_offset(p, m, n + i)];
+      a[i] = kF16 ? __float_as_uint(__uint_as_float(t) + __uint_as_float(a[i])) : a[i] + t;
+    }
+  } else if (p.seed != nullptr) {
     const uint4* s = reinterpret_cast<const uint4*>(static_cast<const uint32_t*>(p.seed) + off);
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
@@ -205,7 +217,13 @@ __device__ __forceinline__ void store16(const ConvKernelParams& p, int m, int n,
     for (int j = 0; j < 4; ++j)
       w[j] = __byte_perm(__byte_perm(b[4 * j], b[4 * j + 1], 0x0040), __byte_perm(b[4 * j + 2], b[4 * j + 3], 0x0040),
                          0x5410);
-    st_v4(static_cast<int8_t*>(p.out) + off, w[0], w[1], w[2], w[3]);
+    if (vec) {
+      st_v4(static_cast<int8_t*>(p.out) + off, w[0], w[1], w[2], w[3]);
+    } else {
+#pragma unroll 1
+      for (int i = 0; i < 16 && n + i < p.Ngemm; ++i)
+        static_cast<uint8_t*>(p.out)[out_offset(p, m, n + i)] = (uint8_t)(b[i] & 0xffu);
+    }
   } else if constexpr (kEpm == EPM_F16) {
     uint32_t w[8];
 #pragma unroll
@@ -213,13 +231,24 @@ __device__ __forceinline__ void store16(const ConvKernelParams& p, int m, int n,
       __half2 h = __floats2half2_rn(__uint_as_float(a[2 * j]), __uint_as_float(a[2 * j + 1]));
       w[j] = *reinterpret_cast<uint32_t*>(&h);
     }
-    uint16_t* o = static_cast<uint16_t*>(p.out) + off;
-    st_v4(o, w[0], w[1], w[2], w[3]);
-    st_v4(o + 8, w[4], w[5], w[6], w[7]);
+    if (vec) {
+      uint16_t* o = static_cast<uint16_t*>(p.out) + off;
+      st_v4(o, w[0], w[1], w[2], w[3]);
+      st_v4(o + 8, w[4], w[5], w[6], w[7]);
+    } else {
+#pragma unroll 1
+      for (int i = 0; i < 16 && n + i < p.Ngemm; ++i)
+        static_cast<uint16_t*>(p.out)[out_offset(p, m, n + i)] = (uint16_t)(w[i >> 1] >> (16 * (i & 1)));
+    }
   } else {  // raw 32-bit accumulator image (i32 / f32)
-    uint32_t* o = static_cast<uint32_t*>(p.out) + off;
+    if (vec) {
+      uint32_t* o = static_cast<uint32_t*>(p.out) + off;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) st_v4(o + 4 * j, a[4 * j], a[4 * j + 1], a[4 * j + 2], a[4 * j + 3]);
+      for (int j = 0; j < 4; ++j) st_v4(o + 4 * j, a[4 * j], a[4 * j + 1], a[4 * j + 2], a[4 * j + 3]);
+    } else {
+#pragma unroll 1
+      for (int i = 0; i < 16 && n + i < p.Ngemm; ++i) static_cast<uint32_t*>(p.out)[out_offset(p, m, n + i)] = a[i];
+    }
   }
 }
 
@@ -409,7 +438,7 @@ __global__ void __launch_bounds__(EpiCfg<BN>::THREADS, 1) conv_tc_kernel(const _
               if (n + 4 * j < p.Ngemm) st_v4(o + 4 * j, v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
           } else {
             if (n < p.Ngemm) store16<kF16, kEpm>(p, m, n, v);
-            if (n + 16 < p.Ngemm) store16<kF16, kEpm>(p, m, n + 16, v + 16);
+            if (n + 16 < p.Ngemm) store16<kF16, kEpm>(p, m, n + 16, v + 16);  // masks a ragged tail
           }
         }
         if (threadIdx.x == 128) TZC_TRACE_POINT(10 + 3 * c);

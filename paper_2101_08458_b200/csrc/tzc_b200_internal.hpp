@@ -36,6 +36,8 @@ struct Problem {
 };
 
 Status plan_problem(const Problem& pb, tzc_plan* plan);
+bool needs_k7(const Problem& pb);
+Problem k7_gemm(const Problem& pb, int* kp_out);
 Status run_problem(const Problem& pb, const void* a, const void* b, const void* seed, void* out,
                    const tzc_epilogue& ep, cudaStream_t stream);
 void set_forced_splits(int s);
