@@ -172,6 +172,20 @@ TZC_API int tzc_b200_run_op(const char* op_tdsl, const char* intrinsic, const ch
                     int32_t n_inputs, const char* const* names, const void* const* host_inputs,
                     void* host_out, int64_t out_bytes);
 
+/* ---- host-library introspection (op text in, text out; no GPU needed) --------- */
+/* parse_compute + infer_types + print_compute (proj/src/compute_op.cpp:285-313). */
+TZC_API int tzc_b200_parse(const char* op_tdsl, char* buf, int64_t buflen);
+/* inspect(): one "<mapping>" line per feasible mapping, in the reference's
+ * order (proj/src/inspector.cpp:178-216); grouped != 0 adds the fused
+ * data-parallel groups this backend maps onto tcgen05's M / N. */
+TZC_API int tzc_b200_inspect(const char* op_tdsl, const char* intrinsic, int32_t grouped, char* buf, int64_t buflen);
+/* tensorize(): chosen mapping, reference schedule text and the kernel plan. */
+TZC_API int tzc_b200_describe(const char* op_tdsl, const char* intrinsic, char* buf, int64_t buflen);
+/* builtin_names(), one per line. */
+TZC_API int tzc_b200_builtins(char* buf, int64_t buflen);
+/* print_intrinsic(resolve_intrinsic(ref)): the .intr text (proj/src/intrinsics.cpp:298-314). */
+TZC_API int tzc_b200_print_intrinsic(const char* intrinsic, char* buf, int64_t buflen);
+
 /* ---- misc --------------------------------------------------------------------- */
 TZC_API const char* tzc_b200_last_error(void);
 /* Number of kernels this library has launched since load (all devices). */

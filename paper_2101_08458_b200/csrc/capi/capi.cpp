@@ -14,6 +14,12 @@ namespace tzcb200 {
 namespace {
 thread_local std::string g_last_error;
 
+}  // namespace
+
+void set_last_error(const std::string& m) { g_last_error = m; }
+
+namespace {
+
 int report(const Status& st) {
   if (!st.ok()) g_last_error = st.msg;
   return st.code;

@@ -55,5 +55,6 @@ Status im2col_pad(const Problem& pb, const void* x, void* a, int kp, cudaStream_
 Status weight_pad(const Problem& pb, const void* w, void* b, int kp, cudaStream_t st);
 
 extern std::atomic<uint64_t> g_launches;
+void set_last_error(const std::string& msg);
 
 }  // namespace tzcb200

@@ -1,0 +1,87 @@
+"""Op-level API (the reference-facing entry point): a .tdsl op text plus an
+instruction (builtin name or .intr path) and HOST numpy buffers, exactly the
+inputs ``tzc verify op.tdsl --intrinsic X`` works from
+(/root/reference/proj/src/cli.cpp:227-283).  Parsing, inspection, tiling and
+the kernel plan are done by the C++ tzc host library inside libtzc_b200.so;
+the tensorized body runs on the B200.  No CPU fallback exists.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import re
+
+import numpy as np
+
+from ._capi import check, lib
+
+NP = {"u8": np.uint8, "i8": np.int8, "u16": np.uint16, "i16": np.int16, "u32": np.uint32, "i32": np.int32,
+      "fp16": np.uint16, "fp32": np.float32}
+
+
+def _text(fn, *args, cap=1 << 16):
+    while True:
+        buf = C.create_string_buffer(cap)
+        rc = fn(*args, buf, cap)
+        if rc == 0:
+            return buf.value.decode()
+        if "buffer too small" in lib().tzc_b200_last_error().decode() and cap < (1 << 26):
+            cap *= 16
+            continue
+        check(rc)
+
+
+def parse(op_text: str) -> str:
+    """parse_compute + infer_types, printed back (print_compute)."""
+    return _text(lib().tzc_b200_parse, op_text.encode())
+
+
+def builtin_names() -> list:
+    return _text(lib().tzc_b200_builtins).split()
+
+
+def print_intrinsic(intrinsic: str) -> str:
+    """The instruction description in the reference's .intr grammar."""
+    return _text(lib().tzc_b200_print_intrinsic, intrinsic.encode())
+
+
+def inspect(op_text: str, intrinsic: str, grouped: bool = False) -> list:
+    """Feasible loop mappings, reference order ("{y->i, k->j}" strings)."""
+    return [ln for ln in _text(lib().tzc_b200_inspect, op_text.encode(), intrinsic.encode(), int(grouped)).splitlines()
+            if ln]
+
+
+def describe(op_text: str, intrinsic: str) -> str:
+    return _text(lib().tzc_b200_describe, op_text.encode(), intrinsic.encode())
+
+
+def declarations(op_text: str):
+    """[(name, dtype, role, shape)] in declaration order."""
+    out = []
+    for m in re.finditer(r"tensor (\w+) : (\w+) \[([\d, ]+)\] (input|output)", op_text):
+        out.append((m.group(1), m.group(2), m.group(4), tuple(int(v) for v in m.group(3).split(","))))
+    return out
+
+
+def run_op(op_text: str, intrinsic: str, inputs: dict, epilogue: str | None = None, out: np.ndarray | None = None):
+    """Execute the tensorized op on the GPU from host buffers.
+
+    ``inputs`` maps tensor names to arrays at the declared element width
+    (fp16 as uint16 bit patterns); accumulate-form ops take the output's
+    initial image under the output's name.  ``epilogue`` is the optional
+    requantize / cast op over the output (fused)."""
+    decl = declarations(op_text)
+    out_decl = next(d for d in decl if d[2] == "output")
+    odt = out_decl[1]
+    if epilogue is not None:
+        odt = next(d for d in declarations(epilogue) if d[2] == "output")[1]
+    if out is None:
+        out = np.empty(out_decl[3], dtype=NP[odt])
+    names = list(inputs)
+    arrs = [np.ascontiguousarray(inputs[n]) for n in names]
+    cn = (C.c_char_p * len(names))(*[n.encode() for n in names])
+    cp = (C.c_void_p * len(names))(*[a.ctypes.data for a in arrs])
+    rc = lib().tzc_b200_run_op(op_text.encode(), intrinsic.encode(),
+                               None if epilogue is None else epilogue.encode(), len(names), cn, cp,
+                               C.c_void_p(out.ctypes.data), out.nbytes)
+    check(rc)
+    return out

@@ -1,0 +1,80 @@
+"""The reference-facing entry (tzc_b200_run_op): op text + instruction +
+HOST buffers, parsed/inspected/planned by the C++ host library and run on the
+B200 — against the reference's own outputs (golden fixtures) and the oracle."""
+import hashlib
+import os
+
+import numpy as np
+import pytest
+
+from oracle.pyoracle import Orc
+from paper_2101_08458_b200 import ops
+from paper_2101_08458_b200.workloads import conv2d_nhwc_tdsl, matmul_tdsl, requant_tdsl
+from tests.gpu_helpers import rel_dev
+from tests.test_oracle import SEEDED, SEEDED_NAMES, decls
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+def instr_for(text, n=64):
+    if "fp16" in text:
+        mn = "_mn" if "B[k, y]" in text else ""
+        return f"tcgen05_f16_m128n{n}k16{mn}"
+    return f"tcgen05_i8_m128n{n}k32"
+
+
+@pytest.mark.parametrize("name", [n for n in SEEDED_NAMES if n.startswith(("mm_", "conv_"))])
+def test_run_op_reference_fixtures(cuda, name):
+    text = str(SEEDED[name + "__text"])
+    ins = Orc.random_inputs(decls(text), int(SEEDED[name + "__seed"]), update=True)
+    got = ops.run_op(text, instr_for(text), ins)
+    want = SEEDED[name + "__out"]
+    if "f16" in name:
+        assert rel_dev(want, got) <= 1e-3
+    else:
+        assert np.array_equal(got, want)
+
+
+def test_run_op_c1_with_fused_requant(cuda):
+    """configs[0] through the op-level API: the reference's exact op text,
+    blocked layouts, accumulate-form seed, fused requant epilogue op."""
+    g = np.load(os.path.join(GOLD, "c1.npz"))
+    text = str(g["text"])
+    ins = Orc.random_inputs(decls(text), int(g["seed"]))
+    out = ops.run_op(text, "tcgen05_i8_m128n64k32", ins)
+    assert hashlib.sha256(out.tobytes()).hexdigest() == str(g["sha_i32"])
+    q = ops.run_op(text, "tcgen05_i8_m128n64k32", ins, epilogue=requant_tdsl(out.shape, 2.0 ** -12, src="out"))
+    assert q.dtype == np.int8
+    assert hashlib.sha256(q.tobytes()).hexdigest() == str(g["sha_i8"])
+
+
+def test_run_op_matmul_requant_and_no_seed(cuda):
+    text = matmul_tdsl(512, 256, 384)
+    ins = Orc.random_inputs(decls(text), 77)
+    ref = Orc.matmul(ins["A"], ins["B"], ins["C"])
+    q = ops.run_op(text, "tcgen05_i8_m128n256k32", ins, epilogue=requant_tdsl((512, 256), 0.0123))
+    assert np.array_equal(q, Orc.requant_i8(ref, np.float32(0.0123)))
+    no_seed = {k: v for k, v in ins.items() if k != "C"}
+    assert np.array_equal(ops.run_op(text, "tcgen05_i8_m128n256k32", no_seed), Orc.matmul(ins["A"], ins["B"]))
+
+
+@pytest.mark.parametrize("n,h,c,k,r,st", [(2, 12, 64, 128, 3, 1), (2, 21, 3, 64, 7, 2), (1, 14, 256, 512, 1, 2)])
+def test_run_op_conv_nhwc(cuda, n, h, c, k, r, st):
+    text = conv2d_nhwc_tdsl(n, h, h, c, k, r, r, st)
+    ins = Orc.random_inputs(decls(text), 5)
+    ref = Orc.conv2d_nhwc(ins["data"], ins["kernel"], st, ins["out"])
+    assert np.array_equal(ops.run_op(text, "tcgen05_i8_m128n64k32", ins), ref)
+
+
+def test_run_op_errors(cuda):
+    from paper_2101_08458_b200._capi import TzcError
+    text = matmul_tdsl(128, 64, 64)
+    ins = Orc.random_inputs(decls(text), 1)
+    with pytest.raises(TzcError) as e:
+        ops.run_op(text, "tcgen05_i8_m128n64k32", {"A": ins["A"]})
+    assert e.value.kind == "MissingInput"
+    with pytest.raises(TzcError) as e:
+        ops.run_op(text, "tcgen05_i8_m128n64k32", ins, epilogue="tensor Z : i32 [2] input\ntensor Q : i8 [2] output\n"
+                   "loop i : dp 2\nQ[i] = cast<i8>(Z[i])\n")
+    assert e.value.kind == "InjectError"
