@@ -30,8 +30,10 @@ def test_library_exports_every_declared_symbol():
     syms = {ln.split()[-1] for ln in out.splitlines() if " T " in ln}
     missing = [f for f in header_functions() if f not in syms]
     assert not missing, missing
-    # nothing else leaks from the shared object (hidden visibility)
-    assert all(s.startswith("tzc_") for s in syms), sorted(s for s in syms if not s.startswith("tzc_"))
+    # nothing else leaks from the shared object: the C ABI plus the tzc::
+    # C++ host-library API (include/tzc/tzc.hpp); kernels/runtime stay hidden
+    leaked = sorted(s for s in syms if not (s.startswith("tzc_") or s.startswith("_ZN3tzc")))
+    assert not leaked, leaked
 
 
 def test_loads_without_gpu_and_reports_no_device():
