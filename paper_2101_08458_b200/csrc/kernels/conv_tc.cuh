@@ -146,24 +146,25 @@ __device__ __forceinline__ uint32_t rne24(uint32_t a) {
 }
 
 // Epilogue of 16 consecutive accumulator columns v[0..16) of row m, column n.
-template <bool kF16, int kEpm>
+template <bool kF16, int kEpm, bool kVec>
 __device__ __forceinline__ void store16(const ConvKernelParams& p, int m, int n, const uint32_t* v) {
   const int64_t off = out_offset(p, m, n);
   // vector path: 16 columns in range and every piece 16-byte aligned (host
   // checked); otherwise element-wise (ragged channel counts, odd strides)
-  const bool vec = p.vec_ok && n + 16 <= p.Ngemm;
+  constexpr bool vec = kVec;  // caller decided per tile: all pieces in range and aligned
   uint32_t a[16];
 #pragma unroll
   for (int i = 0; i < 16; ++i) a[i] = v[i];
-  if (p.seed != nullptr && !vec) {
+  if (!vec && p.seed != nullptr) {
     const uint32_t* sd = static_cast<const uint32_t*>(p.seed);
-#pragma unroll 1
-    for (int i = 0; i < 16; ++i) {
-      if (n + i >= p.Ngemm) break;
-      const uint32_t t = sd[out_offset(p, m, n + i)];
-      a[i] = kF16 ? __float_as_uint(__uint_as_float(t) + __uint_as_float(a[i])) : a[i] + t;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {  // constant indices: a[] stays in registers
+      if (n + i < p.Ngemm) {
+        const uint32_t t = sd[out_offset(p, m, n + i)];
+        a[i] = kF16 ? __float_as_uint(__uint_as_float(t) + __uint_as_float(a[i])) : a[i] + t;
+      }
     }
-  } else if (p.seed != nullptr) {
+  } else if (vec && p.seed != nullptr) {
     const uint4* s = reinterpret_cast<const uint4*>(static_cast<const uint32_t*>(p.seed) + off);
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
@@ -217,12 +218,12 @@ __device__ __forceinline__ void store16(const ConvKernelParams& p, int m, int n,
     for (int j = 0; j < 4; ++j)
       w[j] = __byte_perm(__byte_perm(b[4 * j], b[4 * j + 1], 0x0040), __byte_perm(b[4 * j + 2], b[4 * j + 3], 0x0040),
                          0x5410);
-    if (vec) {
+    if constexpr (vec) {
       st_v4(static_cast<int8_t*>(p.out) + off, w[0], w[1], w[2], w[3]);
     } else {
-#pragma unroll 1
-      for (int i = 0; i < 16 && n + i < p.Ngemm; ++i)
-        static_cast<uint8_t*>(p.out)[out_offset(p, m, n + i)] = (uint8_t)(b[i] & 0xffu);
+#pragma unroll
+      for (int i = 0; i < 16; ++i)
+        if (n + i < p.Ngemm) static_cast<uint8_t*>(p.out)[out_offset(p, m, n + i)] = (uint8_t)(b[i] & 0xffu);
     }
   } else if constexpr (kEpm == EPM_F16) {
     uint32_t w[8];
@@ -231,23 +232,24 @@ __device__ __forceinline__ void store16(const ConvKernelParams& p, int m, int n,
       __half2 h = __floats2half2_rn(__uint_as_float(a[2 * j]), __uint_as_float(a[2 * j + 1]));
       w[j] = *reinterpret_cast<uint32_t*>(&h);
     }
-    if (vec) {
+    if constexpr (vec) {
       uint16_t* o = static_cast<uint16_t*>(p.out) + off;
       st_v4(o, w[0], w[1], w[2], w[3]);
       st_v4(o + 8, w[4], w[5], w[6], w[7]);
     } else {
-#pragma unroll 1
-      for (int i = 0; i < 16 && n + i < p.Ngemm; ++i)
-        static_cast<uint16_t*>(p.out)[out_offset(p, m, n + i)] = (uint16_t)(w[i >> 1] >> (16 * (i & 1)));
+#pragma unroll
+      for (int i = 0; i < 16; ++i)
+        if (n + i < p.Ngemm) static_cast<uint16_t*>(p.out)[out_offset(p, m, n + i)] = (uint16_t)(w[i >> 1] >> (16 * (i & 1)));
     }
   } else {  // raw 32-bit accumulator image (i32 / f32)
-    if (vec) {
+    if constexpr (vec) {
       uint32_t* o = static_cast<uint32_t*>(p.out) + off;
 #pragma unroll
       for (int j = 0; j < 4; ++j) st_v4(o + 4 * j, a[4 * j], a[4 * j + 1], a[4 * j + 2], a[4 * j + 3]);
     } else {
-#pragma unroll 1
-      for (int i = 0; i < 16 && n + i < p.Ngemm; ++i) static_cast<uint32_t*>(p.out)[out_offset(p, m, n + i)] = a[i];
+#pragma unroll
+      for (int i = 0; i < 16; ++i)
+        if (n + i < p.Ngemm) static_cast<uint32_t*>(p.out)[out_offset(p, m, n + i)] = a[i];
     }
   }
 }
@@ -421,27 +423,53 @@ __global__ void __launch_bounds__(EpiCfg<BN>::THREADS, 1) conv_tc_kernel(const _
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       if (threadIdx.x == 128) TZC_TRACE_POINT(5);
+      // whole tile in range and 16-byte aligned: the compact vector epilogue;
+      // otherwise (ragged channels, odd strides) the element-wise one
+      const bool fast = p.vec_ok && (n_tile + 1) * BN <= p.Ngemm;
+      if (p.ep_kind == EP_PARTIAL) {
 #pragma unroll 1
-      for (int c = 0; c < HALF / 32; ++c) {
-        const int col = h * HALF + c * 32;
-        uint32_t v[32];
-        if (threadIdx.x == 128) TZC_TRACE_POINT(8 + 3 * c);
-        tmem_ld32(tmem_base + ((q * 32) << 16) + acc * BN + col, v);
-        tmem_ld_wait();
-        if (threadIdx.x == 128) TZC_TRACE_POINT(9 + 3 * c);
-        const int n = n_tile * BN + col;
-        if (m < p.M) {
-          if (p.ep_kind == EP_PARTIAL) {
+        for (int c = 0; c < HALF / 32; ++c) {
+          const int col = h * HALF + c * 32;
+          uint32_t v[32];
+          tmem_ld32(tmem_base + ((q * 32) << 16) + acc * BN + col, v);
+          tmem_ld_wait();
+          const int n = n_tile * BN + col;
+          if (m < p.M) {
             uint32_t* o = static_cast<uint32_t*>(p.partial) + ((int64_t)split * p.M + m) * p.Ngemm + n;
 #pragma unroll
             for (int j = 0; j < 8; ++j)
               if (n + 4 * j < p.Ngemm) st_v4(o + 4 * j, v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
-          } else {
-            if (n < p.Ngemm) store16<kF16, kEpm>(p, m, n, v);
-            if (n + 16 < p.Ngemm) store16<kF16, kEpm>(p, m, n + 16, v + 16);  // masks a ragged tail
           }
         }
-        if (threadIdx.x == 128) TZC_TRACE_POINT(10 + 3 * c);
+      } else if (fast) {
+#pragma unroll 1
+        for (int c = 0; c < HALF / 32; ++c) {
+          const int col = h * HALF + c * 32;
+          uint32_t v[32];
+          if (threadIdx.x == 128) TZC_TRACE_POINT(8 + 3 * c);
+          tmem_ld32(tmem_base + ((q * 32) << 16) + acc * BN + col, v);
+          tmem_ld_wait();
+          if (threadIdx.x == 128) TZC_TRACE_POINT(9 + 3 * c);
+          const int n = n_tile * BN + col;
+          if (m < p.M) {
+            store16<kF16, kEpm, true>(p, m, n, v);
+            store16<kF16, kEpm, true>(p, m, n + 16, v + 16);
+          }
+          if (threadIdx.x == 128) TZC_TRACE_POINT(10 + 3 * c);
+        }
+      } else {
+#pragma unroll 1
+        for (int c = 0; c < HALF / 32; ++c) {
+          const int col = h * HALF + c * 32;
+          uint32_t v[32];
+          tmem_ld32(tmem_base + ((q * 32) << 16) + acc * BN + col, v);
+          tmem_ld_wait();
+          const int n = n_tile * BN + col;
+          if (m < p.M) {
+            if (n < p.Ngemm) store16<kF16, kEpm, false>(p, m, n, v);
+            if (n + 16 < p.Ngemm) store16<kF16, kEpm, false>(p, m, n + 16, v + 16);
+          }
+        }
       }
       tc_fence_before();
       __syncwarp();
@@ -496,7 +524,10 @@ __global__ void splitk_reduce_kernel(const __grid_constant__ ConvKernelParams p)
         }
       }
     }
-    store16<kF16, kEpm>(p, m, n, v);
+    if (p.vec_ok)
+      store16<kF16, kEpm, true>(p, m, n, v);
+    else
+      store16<kF16, kEpm, false>(p, m, n, v);
   }
 }
 
