@@ -149,6 +149,10 @@ TZC_API int tzc_b200_plan_conv(const tzc_conv_desc* d, tzc_plan* plan);
 TZC_API int tzc_b200_plan_gemm(const tzc_gemm_desc* d, tzc_plan* plan);
 /* Force a split-K factor for subsequent launches (0 = automatic). */
 TZC_API int tzc_b200_set_splits(int32_t splits);
+/* Process-wide options: "splits" (as above), "shifted_window" (1 = use the
+ * weight-stationary shifted-window kernel for eligible stride-1 convs, the
+ * default; 0 = always TMA im2col). */
+TZC_API int tzc_b200_set_option(const char* name, int64_t value);
 
 /* K5 layout adapter for the reference's channel-blocked conv2d_tdsl layouts
  * (cb = 4 rows are below TMA's 16-byte minimum):

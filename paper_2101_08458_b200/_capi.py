@@ -26,7 +26,7 @@ ERROR_KINDS = {
 # Every exported symbol the header declares (checked by tests/test_capi.py).
 EXPORTS = (
     "tzc_b200_conv2d_i8", "tzc_b200_conv2d_f16", "tzc_b200_gemm_i8", "tzc_b200_gemm_f16",
-    "tzc_b200_plan_conv", "tzc_b200_plan_gemm", "tzc_b200_set_splits",
+    "tzc_b200_plan_conv", "tzc_b200_plan_gemm", "tzc_b200_set_splits", "tzc_b200_set_option",
     "tzc_b200_unblock_data", "tzc_b200_unblock_kernel", "tzc_b200_run_op",
     "tzc_b200_parse", "tzc_b200_inspect", "tzc_b200_describe", "tzc_b200_builtins",
     "tzc_b200_print_intrinsic",
@@ -97,6 +97,7 @@ def lib():
             L.tzc_b200_plan_conv.argtypes = [C.POINTER(ConvDesc), C.POINTER(Plan)]
             L.tzc_b200_plan_gemm.argtypes = [C.POINTER(GemmDesc), C.POINTER(Plan)]
             L.tzc_b200_set_splits.argtypes = [C.c_int32]
+            L.tzc_b200_set_option.argtypes = [C.c_char_p, C.c_int64]
             L.tzc_b200_unblock_data.argtypes = [P, P] + [C.c_int32] * 5 + [P]
             L.tzc_b200_unblock_kernel.argtypes = [P, P] + [C.c_int32] * 7 + [P]
             L.tzc_b200_run_op.argtypes = [C.c_char_p, C.c_char_p, C.c_char_p, C.c_int32,

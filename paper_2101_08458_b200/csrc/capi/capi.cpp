@@ -209,6 +209,21 @@ int tzc_b200_plan_gemm(const tzc_gemm_desc* d, tzc_plan* plan) {
   TZC_GUARD_END
 }
 
+int tzc_b200_set_option(const char* name, int64_t value) {
+  if (!name) return report(Status(TZC_E_MISSING_INPUT, "NULL option name"));
+  const std::string n(name);
+  if (n == "splits") {
+    if (value < 0) return report(Status(TZC_E_SHAPE, "splits must be >= 0"));
+    set_forced_splits((int)value);
+    return TZC_OK;
+  }
+  if (n == "shifted_window") {
+    set_ws_enabled(value ? 1 : 0);
+    return TZC_OK;
+  }
+  return report(Status(TZC_E_VALIDATION, "unknown option '" + n + "'"));
+}
+
 int tzc_b200_set_splits(int32_t splits) {
   if (splits < 0) return report(Status(TZC_E_SHAPE, "splits must be >= 0"));
   set_forced_splits(splits);

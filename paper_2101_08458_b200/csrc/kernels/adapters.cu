@@ -185,3 +185,77 @@ Status weight_pad(const Problem& pb, const void* w, void* b, int kp, cudaStream_
 }
 
 }  // namespace tzcb200
+
+// ---- space-to-depth for stride-2 thin-channel convs (the C=3 stem) -------------
+// A stride-2 R x S conv over C channels equals a stride-1 ceil(R/2) x ceil(S/2)
+// conv over the 2x2 space-to-depth input with 4C channels (zero-padded here
+// to 16 so each pixel is one 16-byte row):
+//   x4[n,i,j,(a*2+b)*C+c] = x[n,2i+a,2j+b,c],  w4[k,i,j,(a*2+b)*C+c] = w[k,2i+a,2j+b,c]
+// (out-of-range taps / pixels are zero).  Pure byte moves: exact.
+namespace tzcdev {
+
+__global__ void s2d_data_kernel(const uint8_t* __restrict__ x, uint4* __restrict__ x4, int64_t npix4, int Hp, int Wp,
+                                int C, int Hp4, int Wp4) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < npix4; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t n = i / ((int64_t)Hp4 * Wp4);
+    const int rem = (int)(i - n * Hp4 * Wp4);
+    const int h4 = rem / Wp4, w4 = rem - h4 * Wp4;
+    uint8_t v[16];
+#pragma unroll
+    for (int t = 0; t < 16; ++t) v[t] = 0;
+    for (int a = 0; a < 2; ++a)
+      for (int b = 0; b < 2; ++b) {
+        const int h = 2 * h4 + a, w = 2 * w4 + b;
+        if (h < Hp && w < Wp) {
+          const uint8_t* src = x + ((n * Hp + h) * Wp + w) * C;
+          for (int c = 0; c < C; ++c) v[(a * 2 + b) * C + c] = src[c];
+        }
+      }
+    uint4 o;
+    o.x = v[0] | (v[1] << 8) | (v[2] << 16) | ((uint32_t)v[3] << 24);
+    o.y = v[4] | (v[5] << 8) | (v[6] << 16) | ((uint32_t)v[7] << 24);
+    o.z = v[8] | (v[9] << 8) | (v[10] << 16) | ((uint32_t)v[11] << 24);
+    o.w = v[12] | (v[13] << 8) | (v[14] << 16) | ((uint32_t)v[15] << 24);
+    x4[i] = o;
+  }
+}
+
+__global__ void s2d_weight_kernel(const uint8_t* __restrict__ w, uint8_t* __restrict__ w4, int K, int R, int S, int C,
+                                  int64_t wsk, int64_t wst, int R4, int S4) {
+  const int64_t total = (int64_t)K * R4 * S4 * 16;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int ch = (int)(i % 16);
+    int64_t t = i / 16;
+    const int j = (int)(t % S4);
+    t /= S4;
+    const int ii = (int)(t % R4);
+    const int k = (int)(t / R4);
+    uint8_t v = 0;
+    if (ch < 4 * C) {
+      const int ab = ch / C, c = ch - ab * C;
+      const int r = 2 * ii + ab / 2, s = 2 * j + ab % 2;
+      if (r < R && s < S) v = w[k * wsk + (int64_t)(r * S + s) * wst + c];
+    }
+    w4[i] = v;
+  }
+}
+
+}  // namespace tzcdev
+
+namespace tzcb200 {
+
+Status s2d_stem(const Problem& pb, const void* x, const void* w, void* x4, void* w4, int hp4, int wp4, int r4, int s4,
+                cudaStream_t st) {
+  const int64_t npix4 = (int64_t)pb.n * hp4 * wp4;
+  tzcdev::s2d_data_kernel<<<blocks_for(npix4), 256, 0, st>>>((const uint8_t*)x, (uint4*)x4, npix4, pb.hp, pb.wp, pb.c,
+                                                             hp4, wp4);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  const int64_t nw = (int64_t)pb.ngemm * r4 * s4 * 16;
+  tzcdev::s2d_weight_kernel<<<blocks_for(nw), 256, 0, st>>>((const uint8_t*)w, (uint8_t*)w4, pb.ngemm, pb.r, pb.s, pb.c,
+                                                            pb.w_stride_k, pb.w_stride_tap, r4, s4);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? Status() : Status(TZC_E_DEVICE, cudaGetErrorString(e));
+}
+
+}  // namespace tzcb200

@@ -11,8 +11,10 @@
 #include <cudaTypedefs.h>
 
 #include <atomic>
+#include <map>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -20,6 +22,7 @@
 
 #include "../tzc_b200_internal.hpp"
 #include "conv_tc.cuh"
+#include "conv_ws.cuh"
 
 namespace tzcb200 {
 
@@ -183,30 +186,39 @@ Status enc_check(CUresult r, const char* what) {
   return Status();
 }
 
-// Device scratch, cached per process and slot (0: split-K partials,
-// 1: K7 im2col rows, 2: K7 padded weights); grown outside timed loops.
+// Device scratch, cached per (stream, slot) — slot 0: split-K partials,
+// 1: K7 im2col rows, 2: K7 padded weights.  Per stream so that independent
+// ops captured on parallel graph branches never share scratch; launches on
+// one stream are ordered, so reuse within a stream is safe.  Grown outside
+// timed loops (first use).
 std::mutex g_ws_mu;
-void* g_ws[3] = {nullptr, nullptr, nullptr};
-size_t g_ws_bytes[3] = {0, 0, 0};
+struct Scratch {
+  void* p[3] = {nullptr, nullptr, nullptr};
+  size_t bytes[3] = {0, 0, 0};
+};
+std::map<cudaStream_t, Scratch> g_ws;
 int g_forced_splits = 0;
+int g_ws_enabled = 1;  // shifted-window kernel for eligible stride-1 convs (TZC_B200_NO_WS=1 disables)
 
-Status workspace(int slot, size_t bytes, void** out) {
+Status workspace(int slot, size_t bytes, void** out, cudaStream_t stream) {
   std::lock_guard<std::mutex> lk(g_ws_mu);
-  if (bytes > g_ws_bytes[slot]) {
-    if (g_ws[slot]) cudaFree(g_ws[slot]);
-    g_ws[slot] = nullptr;
-    g_ws_bytes[slot] = 0;
-    cudaError_t e = cudaMalloc(&g_ws[slot], bytes);
+  Scratch& s = g_ws[stream];
+  if (bytes > s.bytes[slot]) {
+    if (s.p[slot]) cudaFree(s.p[slot]);
+    s.p[slot] = nullptr;
+    s.bytes[slot] = 0;
+    cudaError_t e = cudaMalloc(&s.p[slot], bytes);
     if (e != cudaSuccess) return Status(TZC_E_DEVICE, std::string("workspace: ") + cudaGetErrorString(e));
-    g_ws_bytes[slot] = bytes;
+    s.bytes[slot] = bytes;
   }
-  *out = g_ws[slot];
+  *out = s.p[slot];
   return Status();
 }
 
 }  // namespace
 
 void set_forced_splits(int s) { g_forced_splits = s; }
+void set_ws_enabled(int on) { g_ws_enabled = on; }
 
 // ---- K7 (thin-channel) rewrite ------------------------------------------------
 bool needs_k7(const Problem& pb) { return pb.b_kn == 0 && ((int64_t)pb.c * (pb.f16 ? 2 : 1)) % 16 != 0; }
@@ -234,8 +246,36 @@ Problem k7_gemm(const Problem& pb, int* kp_out) {
   return g;
 }
 
+struct WsPlan {
+  int bn = 0, kb = 0, pair = 0, c_blocks = 0, sr = 0, box_rows = 0, a_slots = 0, smem = 0, tiles = 0, grid = 0;
+  int64_t p_rows = 0;
+};
+bool ws_plan(const Problem& pb, bool pair, WsPlan* w);
+bool s2d_eligible(const Problem& pb);
+Problem s2d_problem(const Problem& pb);
+
 // ---- planning ----------------------------------------------------------------
 Status plan_problem(const Problem& pb_in, tzc_plan* plan) {
+  {
+    // the shifted-window kernel (a_mode 2) and the space-to-depth stem (a_mode 3)
+    const bool s2d = needs_k7(pb_in) && s2d_eligible(pb_in);
+    const Problem q = s2d ? s2d_problem(pb_in) : pb_in;
+    WsPlan w;
+    if ((s2d || (!needs_k7(pb_in) && g_ws_enabled)) && ws_plan(q, s2d, &w)) {
+      plan->bm = 128;
+      plan->bn = w.bn;
+      plan->bk_bytes = w.kb;
+      plan->stages = w.a_slots;
+      plan->a_mode = s2d ? 3 : 2;
+      plan->splits = 1;
+      plan->grid = w.grid;
+      plan->smem_bytes = w.smem;
+      plan->tiles_m = w.tiles;
+      plan->tiles_n = 1;
+      plan->workspace_bytes = s2d ? (int64_t)q.n * q.hp * q.wp * 16 : 0;
+      return Status();
+    }
+  }
   int kp = 0;
   const Problem pb = needs_k7(pb_in) ? k7_gemm(pb_in, &kp) : pb_in;
   const int e = pb.f16 ? 2 : 1;
@@ -286,12 +326,239 @@ Status plan_problem(const Problem& pb_in, tzc_plan* plan) {
   return Status();
 }
 
+// Output layout, seed and fused-epilogue fields shared by both kernels.
+void fill_epilogue(ConvKernelParams* pp, const Problem& pb, const void* seed, void* out, const tzc_epilogue& ep);
+// ---- weight-stationary shifted-window path (conv_ws.cuh) --------------------------
+
+namespace {
+
+int ws_smem(const WsPlan& w, int taps) {
+  const int b = ((taps * w.c_blocks * w.bn * w.kb + 1023) / 1024) * 1024;
+  const int a_rows = w.sr > w.box_rows ? 2 * w.box_rows : w.box_rows;
+  const int slot = ((a_rows * w.kb + 1023) / 1024) * 1024;
+  return 1024 + b + w.a_slots * slot + 256;
+}
+
+template <int BN, int KB, bool F16, bool PAIR, int EPM>
+Status launch_ws_kernel(const ConvKernelParams& p, int grid, int smem, cudaStream_t stream) {
+  auto kern = tzcdev::conv_ws_kernel<BN, KB, F16, PAIR, EPM>;
+  static int attr_smem = 0;
+  if (attr_smem < smem) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    if (e != cudaSuccess) return Status(TZC_E_DEVICE, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
+    attr_smem = 227 * 1024;
+  }
+  cudaError_t e = launch_pdl(kern, dim3(grid), dim3(tzcdev::EpiCfg<BN>::THREADS), smem, stream, p);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  if (e == cudaSuccess) e = cudaGetLastError();
+  if (e != cudaSuccess) return Status(TZC_E_DEVICE, std::string("conv_ws launch: ") + cudaGetErrorString(e));
+  return Status();
+}
+
+template <int BN, int KB, bool F16, bool PAIR>
+Status launch_ws_epm(const ConvKernelParams& p, int grid, int smem, cudaStream_t stream) {
+  if (p.ep_kind == tzcdev::EP_REQUANT_I8) {
+    if constexpr (F16) return Status(TZC_E_TYPE, "requant epilogue on an fp16 op");
+    else return launch_ws_kernel<BN, KB, F16, PAIR, tzcdev::EPM_REQUANT>(p, grid, smem, stream);
+  }
+  if (p.ep_kind == tzcdev::EP_CAST_F16) {
+    if constexpr (!F16) return Status(TZC_E_TYPE, "fp16 cast epilogue on an int8 op");
+    else return launch_ws_kernel<BN, KB, F16, PAIR, tzcdev::EPM_F16>(p, grid, smem, stream);
+  }
+  return launch_ws_kernel<BN, KB, F16, PAIR, tzcdev::EPM_RAW>(p, grid, smem, stream);
+}
+
+using WsFn = Status (*)(const ConvKernelParams&, int, int, cudaStream_t);
+
+WsFn ws_fn(int bn, int kb, bool f16, bool pair) {
+#define TZC_WS(BN, KB, F16, PAIR) \
+  if (bn == BN && kb == KB && f16 == F16 && pair == PAIR) return &launch_ws_epm<BN, KB, F16, PAIR>;
+  TZC_WS(64, 64, false, false) TZC_WS(128, 64, false, false) TZC_WS(256, 64, false, false)
+  TZC_WS(64, 128, false, false) TZC_WS(128, 128, false, false) TZC_WS(256, 128, false, false)
+  TZC_WS(64, 16, false, true) TZC_WS(128, 16, false, true) TZC_WS(256, 16, false, true)
+  TZC_WS(64, 64, true, false) TZC_WS(128, 64, true, false) TZC_WS(256, 64, true, false)
+  TZC_WS(64, 128, true, false) TZC_WS(128, 128, true, false) TZC_WS(256, 128, true, false)
+#undef TZC_WS
+  return nullptr;
+}
+
+}  // namespace
+
+// Eligibility + resources of the shifted-window kernel for a stride-1 conv
+// (pair = 16-byte pixels, the space-to-depth stem).
+bool ws_plan(const Problem& pb, bool pair, WsPlan* w) {
+  if (pb.b_kn || pb.stride != 1 || pb.taps < 2 || needs_k7(pb)) return false;
+  if (!(pb.ngemm == 64 || pb.ngemm == 128 || pb.ngemm == 256)) return false;
+  const int e = pb.f16 ? 2 : 1;
+  const int64_t cb = (int64_t)pb.c * e;
+  WsPlan x;
+  x.bn = pb.ngemm;
+  x.pair = pair ? 1 : 0;
+  if (pair) {
+    if (cb != 16 || pb.s % 2 || pb.f16) return false;
+    x.kb = 16;
+  } else {
+    x.kb = cb % 128 == 0 ? 128 : (cb % 64 == 0 ? 64 : 0);
+    if (!x.kb) return false;
+  }
+  x.c_blocks = (int)(cb / x.kb);
+  if ((int64_t)pb.taps * x.c_blocks * x.bn * x.kb > 160 * 1024) return false;  // weights must stay resident
+  x.sr = 128 + (pb.r - 1) * pb.wp + (pb.s - 1);
+  if (x.sr > 512) return false;
+  x.box_rows = x.sr <= 256 ? x.sr : (((x.sr + 1) / 2 + 7) / 8) * 8;
+  // padded-grid waste: (Hp*Wp)/(OH*OW) extra MMA rows
+  if ((double)pb.hp * pb.wp > 1.35 * (double)pb.oh * pb.ow) return false;
+  x.p_rows = (int64_t)pb.n * pb.hp * pb.wp;
+  if (x.p_rows > INT32_MAX - 1024) return false;
+  for (x.a_slots = 6; x.a_slots >= 2; --x.a_slots)
+    if (ws_smem(x, pb.taps) <= 227 * 1024) break;
+  if (x.a_slots < 2) return false;
+  x.smem = ws_smem(x, pb.taps);
+  x.tiles = (int)((x.p_rows + 127) / 128);
+  x.grid = std::min(x.tiles, num_sms());
+  *w = x;
+  return true;
+}
+
+Status run_ws(const Problem& pb, const WsPlan& w, const void* a, const void* b, const void* seed, void* out,
+              const tzc_epilogue& ep, cudaStream_t stream) {
+  const int e = pb.f16 ? 2 : 1;
+  const int KE = w.kb / e;
+  const CUtensorMapDataType dt = pb.f16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_UINT8;
+  const CUtensorMapSwizzle sw = w.kb == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                                : w.kb == 64  ? CU_TENSOR_MAP_SWIZZLE_64B
+                                              : CU_TENSOR_MAP_SWIZZLE_NONE;
+  ConvKernelParams p;
+  std::memset(&p, 0, sizeof(p));
+  Status st;
+  {  // A: the input as a [N*Hp*Wp pixel rows, C] matrix
+    cuuint64_t dims[2] = {(cuuint64_t)pb.c, (cuuint64_t)w.p_rows};
+    cuuint64_t strides[1] = {(cuuint64_t)pb.c * e};
+    cuuint32_t box[2] = {(cuuint32_t)KE, (cuuint32_t)w.box_rows};
+    cuuint32_t es[2] = {1, 1};
+    st = enc_check(p_encode_tiled(&p.tmA, dt, 2, const_cast<void*>(a), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                  sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE),
+                   "cuTensorMapEncodeTiled(ws A)");
+    if (!st.ok()) return st;
+  }
+  {  // B: (c, k_out, tap); the pair kernel takes two taps per box
+    const int64_t sk = pb.w_stride_k * e, stap = pb.w_stride_tap * e;
+    cuuint64_t dims[3] = {(cuuint64_t)pb.c, (cuuint64_t)pb.ngemm, (cuuint64_t)pb.taps};
+    cuuint64_t strides[2] = {(cuuint64_t)sk, (cuuint64_t)stap};
+    cuuint32_t box[3] = {(cuuint32_t)KE, (cuuint32_t)w.bn, (cuuint32_t)(w.pair ? 2 : 1)};
+    cuuint32_t es[3] = {1, 1, 1};
+    st = enc_check(p_encode_tiled(&p.tmB, dt, 3, const_cast<void*>(b), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                  sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE),
+                   "cuTensorMapEncodeTiled(ws B)");
+    if (!st.ok()) return st;
+  }
+  p.M = (int32_t)pb.m;
+  p.Ngemm = pb.ngemm;
+  p.c_blocks = w.c_blocks;
+  p.S = pb.s;
+  p.R = pb.r;
+  p.Hp = pb.hp;
+  p.Wp = pb.wp;
+  p.OH = pb.oh;
+  p.OWv = pb.ow;
+  p.P = (int32_t)w.p_rows;
+  p.SR = w.sr;
+  p.box_rows = w.box_rows;
+  p.num_tiles = w.tiles;
+  p.splits = w.a_slots;  // ring depth (the kernel has no split-K)
+  fill_epilogue(&p, pb, seed, out, ep);
+  WsFn fn = ws_fn(w.bn, w.kb, pb.f16 != 0, w.pair != 0);
+  if (!fn) return Status(TZC_E_INTERNAL, "no conv_ws instantiation");
+  return fn(p, w.grid, w.smem, stream);
+}
+
+// Space-to-depth geometry for a stride-2 conv with 4*C*e <= 16 (the stem).
+bool s2d_eligible(const Problem& pb) {
+  return pb.stride == 2 && !pb.f16 && !pb.b_kn && pb.c * 4 <= 16 && pb.r > 1 &&
+         (pb.ngemm == 64 || pb.ngemm == 128 || pb.ngemm == 256);
+}
+
+Problem s2d_problem(const Problem& pb) {
+  Problem q = pb;
+  q.hp = (pb.hp + 1) / 2;
+  q.wp = (pb.wp + 1) / 2;
+  q.c = 16;
+  q.r = (pb.r + 1) / 2;
+  q.s = (pb.s + 1) / 2;
+  q.stride = 1;
+  q.taps = q.r * q.s;
+  q.w_stride_k = (int64_t)q.r * q.s * 16;
+  q.w_stride_tap = 16;
+  q.a_mode = tzcdev::A_IM2COL;
+  // oh / ow / m stay the original op's: the epilogue keeps rows with oh < OH, ow < OW
+  return q;
+}
+
+// Output layout, seed and fused-epilogue fields shared by both kernels.
+void fill_epilogue(ConvKernelParams* pp, const Problem& pb, const void* seed, void* out, const tzc_epilogue& ep) {
+  ConvKernelParams& p = *pp;
+  p.out = out;
+  p.seed = seed;
+  p.out_nb = pb.out.nb;
+  p.out_stride_m = pb.out.stride_m;
+  p.out_stride_blk = pb.out.stride_blk;
+  p.ep_kind = ep.kind;
+  p.scale = ep.scale;
+  {
+    // vectorised epilogue: every 16-column piece of out / seed starts 16-byte aligned
+    const int eo = (ep.kind == tzcdev::EP_REQUANT_I8) ? 1 : (ep.kind == tzcdev::EP_CAST_F16) ? 2 : 4;
+    auto al = [](int64_t elems, int eb) { return (elems * eb) % 16 == 0; };
+    bool ok = pb.ngemm % 16 == 0 && (pb.out.nb % 16 == 0) && al(pb.out.stride_m, eo) && al(pb.out.stride_blk, eo) &&
+              reinterpret_cast<uintptr_t>(out) % 16 == 0;
+    if (seed) ok = ok && al(pb.out.stride_m, 4) && al(pb.out.stride_blk, 4) && reinterpret_cast<uintptr_t>(seed) % 16 == 0;
+    p.vec_ok = ok ? 1 : 0;
+  }
+  p.pow2_k = -1;
+  // |seed + sum| < 2^24 is guaranteed without a seed when K*255*128 < 2^24
+  // (u8 x i8 products): the requant then needs no RNE24 range check.
+  p.range_check = (seed != nullptr || pb.f16 || (int64_t)pb.c * pb.taps * 255 * 128 >= (1 << 24)) ? 1 : 0;
+  {
+    // exact power-of-two scale 2^-k, k in [0, 126]: integer requant path
+    int ex = 0;
+    const float fr = std::frexp(ep.scale, &ex);  // scale = fr * 2^ex, fr in [0.5, 1)
+    if (fr == 0.5f && ex - 1 <= 0 && ex - 1 >= -24) p.pow2_k = -(ex - 1);
+  }
+  p.simple = (ep.kind == tzcdev::EP_REQUANT_I8 && p.pow2_k >= 1 && !p.range_check && seed == nullptr && p.vec_ok &&
+              pb.out.nb == pb.ngemm)
+                 ? 1
+                 : 0;
+}
+
 // ---- launch --------------------------------------------------------------------
 Status run_problem(const Problem& pb, const void* a, const void* b, const void* seed, void* out,
                    const tzc_epilogue& ep, cudaStream_t stream) {
   if (!device_ok()) return Status(TZC_E_DEVICE, "no usable sm_100 (B200) device");
   Status st = load_driver();
   if (!st.ok()) return st;
+  static const bool env_no_ws = [] {
+    if (std::getenv("TZC_B200_NO_WS")) g_ws_enabled = 0;
+    return true;
+  }();
+  (void)env_no_ws;
+  if (needs_k7(pb) && s2d_eligible(pb)) {
+    // the stem: space-to-depth to 16-byte pixels, then the shifted-window
+    // kernel in pair mode (two taps per K=32 MMA)
+    const Problem q = s2d_problem(pb);
+    WsPlan w;
+    if (ws_plan(q, true, &w)) {
+      void* x4 = nullptr;
+      void* w4 = nullptr;
+      st = workspace(1, (size_t)q.n * q.hp * q.wp * 16, &x4, stream);
+      if (st.ok()) st = workspace(2, (size_t)q.ngemm * q.taps * 16, &w4, stream);
+      if (st.ok()) st = s2d_stem(pb, a, b, x4, w4, q.hp, q.wp, q.r, q.s, stream);
+      if (st.ok()) st = run_ws(q, w, x4, w4, seed, out, ep, stream);
+      return st;
+    }
+  }
+  if (!needs_k7(pb)) {
+    WsPlan w;
+    if (g_ws_enabled && ws_plan(pb, false, &w)) return run_ws(pb, w, a, b, seed, out, ep, stream);
+  }
   if (needs_k7(pb)) {
     // K7: channel runs too thin for TMA (the C=3 stem).  Materialise
     // zero-padded im2col rows + weights and run them as a GEMM.
@@ -300,8 +567,8 @@ Status run_problem(const Problem& pb, const void* a, const void* b, const void* 
     const int e = pb.f16 ? 2 : 1;
     void* wa = nullptr;
     void* wb = nullptr;
-    st = workspace(1, (size_t)pb.m * kp * e, &wa);
-    if (st.ok()) st = workspace(2, (size_t)pb.ngemm * kp * e, &wb);
+    st = workspace(1, (size_t)pb.m * kp * e, &wa, stream);
+    if (st.ok()) st = workspace(2, (size_t)pb.ngemm * kp * e, &wb, stream);
     if (st.ok()) st = im2col_pad(pb, a, wa, kp, stream);
     if (st.ok()) st = weight_pad(pb, b, wb, kp, stream);
     if (!st.ok()) return st;
@@ -379,34 +646,9 @@ Status run_problem(const Problem& pb, const void* a, const void* b, const void* 
   p.tiles_n = plan.tiles_n;
   p.num_tiles = plan.tiles_m * plan.tiles_n;
   p.splits = plan.splits;
-  p.out = out;
-  p.seed = seed;
-  p.out_nb = pb.out.nb;
-  p.out_stride_m = pb.out.stride_m;
-  p.out_stride_blk = pb.out.stride_blk;
-  p.ep_kind = ep.kind;
-  p.scale = ep.scale;
-  {
-    // vectorised epilogue: every 16-column piece of out / seed starts 16-byte aligned
-    const int eo = (ep.kind == tzcdev::EP_REQUANT_I8) ? 1 : (ep.kind == tzcdev::EP_CAST_F16) ? 2 : 4;
-    auto al = [](int64_t elems, int eb) { return (elems * eb) % 16 == 0; };
-    bool ok = pb.ngemm % 16 == 0 && (pb.out.nb % 16 == 0) && al(pb.out.stride_m, eo) && al(pb.out.stride_blk, eo) &&
-              reinterpret_cast<uintptr_t>(out) % 16 == 0;
-    if (seed) ok = ok && al(pb.out.stride_m, 4) && al(pb.out.stride_blk, 4) && reinterpret_cast<uintptr_t>(seed) % 16 == 0;
-    p.vec_ok = ok ? 1 : 0;
-  }
-  p.pow2_k = -1;
-  // |seed + sum| < 2^24 is guaranteed without a seed when K*255*128 < 2^24
-  // (u8 x i8 products): the requant then needs no RNE24 range check.
-  p.range_check = (seed != nullptr || pb.f16 || (int64_t)pb.c * pb.taps * 255 * 128 >= (1 << 24)) ? 1 : 0;
-  {
-    // exact power-of-two scale 2^-k, k in [0, 126]: integer requant path
-    int ex = 0;
-    const float fr = std::frexp(ep.scale, &ex);  // scale = fr * 2^ex, fr in [0.5, 1)
-    if (fr == 0.5f && ex - 1 <= 0 && ex - 1 >= -24) p.pow2_k = -(ex - 1);
-  }
+  fill_epilogue(&p, pb, seed, out, ep);
   if (plan.splits > 1) {
-    st = workspace(0, (size_t)plan.workspace_bytes, &p.partial);
+    st = workspace(0, (size_t)plan.workspace_bytes, &p.partial, stream);
     if (!st.ok()) return st;
   }
   const Entry* ent = find_entry(plan.bn, plan.bk_bytes, pb.f16, pb.a_mode, pb.b_kn);

@@ -69,6 +69,12 @@ struct alignas(64) ConvKernelParams {
   int32_t pow2_k;       // scale == 2^-pow2_k exactly (>= 0), else -1
   int32_t vec_ok;       // 16-column output/seed pieces are 16-byte aligned
   int32_t range_check;  // 0 when |seed + sum| < 2^24 is guaranteed (no seed, K*255*128 < 2^24)
+  // shifted-window (weight-stationary) mode: padded pixel grid geometry
+  int32_t Hp, Wp, OH, OWv, R;  // OWv: valid output columns
+  int32_t P;                   // padded rows = N * Hp * Wp
+  int32_t SR;                  // A super-tile rows = 128 + (R-1)*Wp + (S-1)
+  int32_t box_rows;            // rows per A TMA box (SR split in <= 2 boxes of <= 256)
+  int32_t simple;              // requant, 2^-k (k>=1), no seed, no range check, row-major, aligned
 };
 
 template <int BN, int KB>
@@ -258,11 +264,62 @@ __device__ __forceinline__ void store16(const ConvKernelParams& p, int m, int n,
 // when BN >= 128: 4 warps per SMSP hide the tcgen05.ld / STG latency).
 template <int BN>
 struct EpiCfg {
-  static constexpr int WARPS = BN >= 128 ? 16 : 8;
+  static constexpr int WARPS = 16;
   static constexpr int GROUPS = WARPS / 4;     // column groups per lane quarter
-  static constexpr int COLS = BN / GROUPS;     // columns per epilogue warp (multiple of 32)
+  static constexpr int COLS = BN / GROUPS;     // columns per epilogue warp (16, 32 or 64)
+  static constexpr int CW = COLS < 32 ? COLS : 32;  // columns per tcgen05.ld chunk
   static constexpr int THREADS = 128 + 32 * WARPS;
 };
+
+// The bench / serving case in a few instructions per element: requant by
+// 2^-k with no seed and |acc| < 2^24 guaranteed (host-checked), row-major
+// 16-byte-aligned output.  trunc(c / 2^k) = (c + ((c >> 31) >>> (32-k))) >> k.
+template <int CW>
+__device__ __forceinline__ void epi_simple(const ConvKernelParams& p, int m, int n, const uint32_t* v) {
+  const int k = p.pow2_k;
+  int8_t* o = static_cast<int8_t*>(p.out) + (int64_t)m * p.out_stride_m + n;
+#pragma unroll
+  for (int j = 0; j < CW / 16; ++j) {
+    uint32_t b[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const int32_t c = (int32_t)v[16 * j + i];
+      b[i] = (uint32_t)((c + (int32_t)((uint32_t)(c >> 31) >> (32 - k))) >> k);
+    }
+    uint32_t w[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      w[q] = __byte_perm(__byte_perm(b[4 * q], b[4 * q + 1], 0x0040), __byte_perm(b[4 * q + 2], b[4 * q + 3], 0x0040),
+                         0x5410);
+    st_v4(o + 16 * j, w[0], w[1], w[2], w[3]);
+  }
+}
+
+// One tcgen05.ld chunk of CW accumulator columns for row m (m < 0: no row).
+template <int CW, bool kF16, int kEpm>
+__device__ __forceinline__ void epi_chunk(const ConvKernelParams& p, uint32_t taddr, int m, int n, bool fast) {
+  uint32_t v[CW];
+  if constexpr (CW == 16)
+    tmem_ld16(taddr, v);
+  else
+    tmem_ld32(taddr, v);
+  tmem_ld_wait();
+  if (m < 0) return;
+  if constexpr (kEpm == EPM_REQUANT) {
+    if (p.simple) {
+      epi_simple<CW>(p, m, n, v);
+      return;
+    }
+  }
+  if (fast) {
+#pragma unroll
+    for (int j = 0; j < CW / 16; ++j) store16<kF16, kEpm, true>(p, m, n + 16 * j, v + 16 * j);
+  } else {
+#pragma unroll
+    for (int j = 0; j < CW / 16; ++j)
+      if (n + 16 * j < p.Ngemm) store16<kF16, kEpm, false>(p, m, n + 16 * j, v + 16 * j);
+  }
+}
 
 template <int BN, int KB, bool kF16, int kAMode, bool kBMN, int kEpm>
 __global__ void __launch_bounds__(EpiCfg<BN>::THREADS, 1) conv_tc_kernel(const __grid_constant__ ConvKernelParams p) {
@@ -427,48 +484,33 @@ __global__ void __launch_bounds__(EpiCfg<BN>::THREADS, 1) conv_tc_kernel(const _
       // otherwise (ragged channels, odd strides) the element-wise one
       const bool fast = p.vec_ok && (n_tile + 1) * BN <= p.Ngemm;
       if (p.ep_kind == EP_PARTIAL) {
+        constexpr int CW = EpiCfg<BN>::CW;
 #pragma unroll 1
-        for (int c = 0; c < HALF / 32; ++c) {
-          const int col = h * HALF + c * 32;
-          uint32_t v[32];
-          tmem_ld32(tmem_base + ((q * 32) << 16) + acc * BN + col, v);
+        for (int c = 0; c < HALF / CW; ++c) {
+          const int col = h * HALF + c * CW;
+          uint32_t v[CW];
+          if constexpr (CW == 16)
+            tmem_ld16(tmem_base + ((q * 32) << 16) + acc * BN + col, v);
+          else
+            tmem_ld32(tmem_base + ((q * 32) << 16) + acc * BN + col, v);
           tmem_ld_wait();
           const int n = n_tile * BN + col;
           if (m < p.M) {
             uint32_t* o = static_cast<uint32_t*>(p.partial) + ((int64_t)split * p.M + m) * p.Ngemm + n;
 #pragma unroll
-            for (int j = 0; j < 8; ++j)
+            for (int j = 0; j < CW / 4; ++j)
               if (n + 4 * j < p.Ngemm) st_v4(o + 4 * j, v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
           }
         }
-      } else if (fast) {
-#pragma unroll 1
-        for (int c = 0; c < HALF / 32; ++c) {
-          const int col = h * HALF + c * 32;
-          uint32_t v[32];
-          if (threadIdx.x == 128) TZC_TRACE_POINT(8 + 3 * c);
-          tmem_ld32(tmem_base + ((q * 32) << 16) + acc * BN + col, v);
-          tmem_ld_wait();
-          if (threadIdx.x == 128) TZC_TRACE_POINT(9 + 3 * c);
-          const int n = n_tile * BN + col;
-          if (m < p.M) {
-            store16<kF16, kEpm, true>(p, m, n, v);
-            store16<kF16, kEpm, true>(p, m, n + 16, v + 16);
-          }
-          if (threadIdx.x == 128) TZC_TRACE_POINT(10 + 3 * c);
-        }
       } else {
+        constexpr int CW = EpiCfg<BN>::CW;
 #pragma unroll 1
-        for (int c = 0; c < HALF / 32; ++c) {
-          const int col = h * HALF + c * 32;
-          uint32_t v[32];
-          tmem_ld32(tmem_base + ((q * 32) << 16) + acc * BN + col, v);
-          tmem_ld_wait();
-          const int n = n_tile * BN + col;
-          if (m < p.M) {
-            if (n < p.Ngemm) store16<kF16, kEpm, false>(p, m, n, v);
-            if (n + 16 < p.Ngemm) store16<kF16, kEpm, false>(p, m, n + 16, v + 16);
-          }
+        for (int c = 0; c < HALF / CW; ++c) {
+          const int col = h * HALF + c * CW;
+          if (threadIdx.x == 128) TZC_TRACE_POINT(8 + 3 * c);
+          epi_chunk<CW, kF16, kEpm>(p, tmem_base + ((q * 32) << 16) + acc * BN + col, m < p.M ? m : -1,
+                                    n_tile * BN + col, fast);
+          if (threadIdx.x == 128) TZC_TRACE_POINT(10 + 3 * c);
         }
       }
       tc_fence_before();

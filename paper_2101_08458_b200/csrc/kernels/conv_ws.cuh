@@ -1,0 +1,213 @@
+// Weight-stationary, shifted-window tcgen05 kernel for stride-1 convolutions
+// (and the C=3 stem after a space-to-depth rewrite).
+//
+// Computing on the *padded* pixel grid q = (n*Hp + oh)*Wp + ow turns every
+// filter tap (r, s) into a row shift of one matrix: the A rows of tap (r, s)
+// for pixels [q0, q0+128) are input pixels [q0 + r*Wp + s, ...).  So one TMA
+// load of SR = 128 + (R-1)*Wp + (S-1) input rows per channel block feeds all
+// R*S taps; each tap is a UMMA descriptor whose start address is shifted by
+// whole rows (hardware-verified for SWIZZLE_128B/64B: the swizzle follows the
+// absolute SMEM address, tools/desc_probe.cu).  The im2col path re-streams
+// every input pixel R*S times through L2; this one streams it ~1.x times.
+// The (R-1) extra columns / rows of the padded grid are computed and dropped
+// by the epilogue (waste (Hp*Wp)/(OH*OW): 7% at 56x56, 15% at 28x28).
+//
+// The whole weight tensor (all taps, all channel blocks, N <= 256) is loaded
+// into SMEM once per CTA and stays there for every tile (weight-stationary):
+// per tile only the A super-tile moves.
+//
+// Pair mode (kPair): 16-byte pixels (the space-to-depth stem: 4 x 4 taps of
+// 12(+4) channels).  SWIZZLE_NONE rows at 16-byte pitch; one K=32 MMA covers
+// taps (r, s) and (r, s+1) by setting the descriptor's leading-byte offset
+// to 16 B — the next row — (hardware-verified, tools/desc_probe.cu).
+#pragma once
+#include "conv_tc.cuh"
+
+namespace tzcdev {
+
+// smem descriptor, SWIZZLE_NONE K-major: LBO = distance between the two
+// 16-byte K chunks of an MMA, SBO = distance between 8-row groups.
+__device__ __forceinline__ uint64_t smem_desc_none(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFF);
+  d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFF) << 16;
+  d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFF) << 32;
+  d |= static_cast<uint64_t>(1) << 46;
+  return d;
+}
+
+template <int BN, int KB, bool kF16, bool kPair, int kEpm>
+__global__ void __launch_bounds__(EpiCfg<BN>::THREADS, 1) conv_ws_kernel(const __grid_constant__ ConvKernelParams p) {
+  constexpr int BM = 128;
+  constexpr int KE = kF16 ? KB / 2 : KB;
+  constexpr uint32_t IDESC = kF16 ? idesc_f16(BM, BN, false) : idesc_i8(BM, BN);
+  constexpr uint32_t TMEM_COLS = ConvCfg<BN, KB>::TMEM_COLS;
+  const int taps = p.R * p.S;
+  const int c_blocks = p.c_blocks;
+  const int b_tile = BN * KB;                                     // one (tap, channel block) of weights
+  const int b_bytes = taps * c_blocks * b_tile;
+  const int a_rows = p.SR > p.box_rows ? 2 * p.box_rows : p.box_rows;  // rows the TMA boxes write
+  const int a_slot = ((a_rows * KB + 1023) / 1024) * 1024;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sB = smem;
+  uint8_t* sA = smem + ((b_bytes + 1023) / 1024) * 1024;
+  const int a_slots = p.splits;  // host-chosen ring depth (stored in `splits`; no split-K in this kernel)
+  uint64_t* afull = reinterpret_cast<uint64_t*>(sA + a_slots * a_slot);
+  uint64_t* aempty = afull + a_slots;
+  uint64_t* bfull = aempty + a_slots;
+  uint64_t* tfull = bfull + 1;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const uint32_t warp = warp_id();
+  const uint32_t lane = threadIdx.x & 31;
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&p.tmA);
+    tma_prefetch(&p.tmB);
+  }
+  if (warp == 1 && lane == 0) {
+    for (int s = 0; s < a_slots; ++s) {
+      mbar_init(&afull[s], 1);
+      mbar_init(&aempty[s], 1);
+    }
+    mbar_init(bfull, 1);
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], EpiCfg<BN>::WARPS);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc<TMEM_COLS>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  pdl_launch_dependents();
+  pdl_wait();
+
+  const int num_tiles = p.num_tiles;
+  if (warp == 0) {
+    if (lane == 0) {
+      // stationary weights: every (tap, channel block) tile, once
+      mbar_expect_tx(bfull, b_bytes);
+      if constexpr (kPair) {
+        for (int t = 0; t < taps; t += 2)  // box (16 ch, BN, 2 taps) == [tap][n][16 B]
+          tma_load_3d(sB + t * b_tile, &p.tmB, bfull, 0, 0, t);
+      } else {
+        for (int t = 0; t < taps; ++t)
+          for (int cb = 0; cb < c_blocks; ++cb) tma_load_3d(sB + (t * c_blocks + cb) * b_tile, &p.tmB, bfull, cb * KE, 0, t);
+      }
+      int slot = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        const int q0 = tile * BM;
+        for (int cb = 0; cb < c_blocks; ++cb) {
+          mbar_wait(&aempty[slot], phase ^ 1);
+          uint8_t* dA = sA + slot * a_slot;
+          mbar_expect_tx(&afull[slot], a_rows * KB);
+          tma_load_2d(dA, &p.tmA, &afull[slot], cb * KE, q0);
+          if (p.SR > p.box_rows) tma_load_2d(dA + p.box_rows * KB, &p.tmA, &afull[slot], cb * KE, q0 + p.box_rows);
+          if (++slot == a_slots) {
+            slot = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ===================== MMA issuer =====================
+    mbar_wait(bfull, 0);
+    int slot = 0;
+    uint32_t phase = 0;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    const uint32_t b_base = smem_u32(sB);
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      mbar_wait(&tempty[acc], acc_phase ^ 1);
+      tc_fence_after();
+      const uint32_t tmem_d = tmem_base + acc * BN;
+      for (int cb = 0; cb < c_blocks; ++cb) {
+        mbar_wait(&afull[slot], phase);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t a_base = smem_u32(sA + slot * a_slot);
+          if constexpr (kPair) {
+            for (int r = 0; r < p.R; ++r)
+              for (int s = 0; s < p.S; s += 2) {
+                const uint32_t shift = (uint32_t)(r * p.Wp + s);
+                const uint64_t ad = smem_desc_none(a_base + shift * 16, 16, 128);
+                const uint64_t bd = smem_desc_none(b_base + (r * p.S + s) * b_tile, BN * 16, 128);
+                umma<kF16>(tmem_d, ad, bd, IDESC, (cb > 0 || r > 0 || s > 0) ? 1u : 0u);
+              }
+          } else {
+            for (int r = 0; r < p.R; ++r)
+              for (int s = 0; s < p.S; ++s) {
+                const uint32_t shift = (uint32_t)(r * p.Wp + s) * KB;
+                const uint32_t bt = b_base + ((r * p.S + s) * c_blocks + cb) * b_tile;
+#pragma unroll
+                for (int k = 0; k < KB / 32; ++k) {
+                  const uint64_t ad = smem_desc_kmajor(a_base + shift + 32 * k, KB);
+                  const uint64_t bd = smem_desc_kmajor(bt + 32 * k, KB);
+                  umma<kF16>(tmem_d, ad, bd, IDESC, (cb > 0 || r > 0 || s > 0 || k > 0) ? 1u : 0u);
+                }
+              }
+          }
+          umma_commit(&aempty[slot]);
+          if (cb == c_blocks - 1) umma_commit(&tfull[acc]);
+        }
+        __syncwarp();
+        if (++slot == a_slots) {
+          slot = 0;
+          phase ^= 1;
+        }
+      }
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+    }
+  } else if (warp >= 4) {
+    // ===================== epilogue: padded grid -> output rows =====================
+    const uint32_t q4 = warp & 3;
+    const uint32_t h = (warp - 4) >> 2;
+    constexpr int COLS = EpiCfg<BN>::COLS;
+    const int hw = p.Hp * p.Wp;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      const int q = tile * BM + q4 * 32 + lane;
+      int m = -1;
+      if (q < p.P) {
+        const int n = q / hw, rem = q - n * hw;
+        const int oh = rem / p.Wp, ow = rem - oh * p.Wp;
+        if (oh < p.OH && ow < p.OWv) m = (n * p.OH + oh) * p.OWv + ow;
+      }
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      {
+        constexpr int CW = EpiCfg<BN>::CW;
+        const bool fast = p.vec_ok && BN <= p.Ngemm;
+#pragma unroll 1
+        for (int c = 0; c < COLS / CW; ++c)
+          epi_chunk<CW, kF16, kEpm>(p, tmem_base + ((q4 * 32) << 16) + acc * BN + h * COLS + c * CW, m,
+                                    h * COLS + c * CW, fast);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+    }
+  }
+  __syncwarp();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc<TMEM_COLS>(tmem_base);
+  }
+}
+
+}  // namespace tzcdev

@@ -41,6 +41,7 @@ Problem k7_gemm(const Problem& pb, int* kp_out);
 Status run_problem(const Problem& pb, const void* a, const void* b, const void* seed, void* out,
                    const tzc_epilogue& ep, cudaStream_t stream);
 void set_forced_splits(int s);
+void set_ws_enabled(int on);
 int device_ok();
 int num_sms();
 
@@ -53,6 +54,9 @@ Status unblock_kernel(const void* src, void* dst, int k, int c, int r, int s, in
 
 Status im2col_pad(const Problem& pb, const void* x, void* a, int kp, cudaStream_t st);
 Status weight_pad(const Problem& pb, const void* w, void* b, int kp, cudaStream_t st);
+
+Status s2d_stem(const Problem& pb, const void* x, const void* w, void* x4, void* w4, int hp4, int wp4, int r4, int s4,
+                cudaStream_t st);
 
 extern std::atomic<uint64_t> g_launches;
 void set_last_error(const std::string& msg);

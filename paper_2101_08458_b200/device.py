@@ -113,5 +113,9 @@ def set_splits(n: int):
     check(lib().tzc_b200_set_splits(n))
 
 
+def set_option(name: str, value: int):
+    check(lib().tzc_b200_set_option(name.encode(), int(value)))
+
+
 def launch_count() -> int:
     return int(lib().tzc_b200_launch_count())
