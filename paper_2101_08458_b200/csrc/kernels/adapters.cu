@@ -194,30 +194,54 @@ Status weight_pad(const Problem& pb, const void* w, void* b, int kp, cudaStream_
 // (out-of-range taps / pixels are zero).  Pure byte moves: exact.
 namespace tzcdev {
 
+// One thread per 16-byte S2D pixel.  For C = 3 with an even row pitch each
+// (a, row) contributes 6 contiguous bytes at an even offset: three 16-bit
+// loads; otherwise byte loads.
 __global__ void s2d_data_kernel(const uint8_t* __restrict__ x, uint4* __restrict__ x4, int64_t npix4, int Hp, int Wp,
                                 int C, int Hp4, int Wp4) {
+  const bool fast3 = C == 3 && ((int64_t)Wp * 3) % 2 == 0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < npix4; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t n = i / ((int64_t)Hp4 * Wp4);
     const int rem = (int)(i - n * Hp4 * Wp4);
     const int h4 = rem / Wp4, w4 = rem - h4 * Wp4;
-    uint8_t v[16];
+    uint32_t wd[4] = {0, 0, 0, 0};
+    if (fast3) {
+      uint32_t u[6] = {0, 0, 0, 0, 0, 0};  // 16-bit pieces: row a -> u[3a..3a+2]
 #pragma unroll
-    for (int t = 0; t < 16; ++t) v[t] = 0;
-    for (int a = 0; a < 2; ++a)
-      for (int b = 0; b < 2; ++b) {
-        const int h = 2 * h4 + a, w = 2 * w4 + b;
-        if (h < Hp && w < Wp) {
-          const uint8_t* src = x + ((n * Hp + h) * Wp + w) * C;
-          for (int c = 0; c < C; ++c) v[(a * 2 + b) * C + c] = src[c];
-        }
+      for (int a = 0; a < 2; ++a) {
+        const int h = 2 * h4 + a;
+        if (h >= Hp) continue;
+        const uint16_t* src = reinterpret_cast<const uint16_t*>(x + ((n * Hp + h) * Wp + 2 * w4) * 3);
+        const bool two = 2 * w4 + 1 < Wp;
+        u[3 * a + 0] = __ldg(src);
+        u[3 * a + 1] = __ldg(src + 1);
+        u[3 * a + 2] = two ? __ldg(src + 2) : 0u;
+        if (!two) u[3 * a + 1] &= 0x00ffu;  // pixel (2*w4+1) is outside the input
       }
-    uint4 o;
-    o.x = v[0] | (v[1] << 8) | (v[2] << 16) | ((uint32_t)v[3] << 24);
-    o.y = v[4] | (v[5] << 8) | (v[6] << 16) | ((uint32_t)v[7] << 24);
-    o.z = v[8] | (v[9] << 8) | (v[10] << 16) | ((uint32_t)v[11] << 24);
-    o.w = v[12] | (v[13] << 8) | (v[14] << 16) | ((uint32_t)v[15] << 24);
-    x4[i] = o;
+      // channel order (a*2+b)*3+c: bytes 0..5 = row 0 (b=0,1), bytes 6..11 = row 1
+      wd[0] = u[0] | (u[1] << 16);
+      wd[1] = u[2] | (u[3] << 16);
+      wd[2] = u[4] | (u[5] << 16);
+    } else {
+      uint8_t v[16];
+#pragma unroll
+      for (int t = 0; t < 16; ++t) v[t] = 0;
+      for (int a = 0; a < 2; ++a)
+        for (int b = 0; b < 2; ++b) {
+          const int h = 2 * h4 + a, w = 2 * w4 + b;
+          if (h < Hp && w < Wp) {
+            const uint8_t* src = x + ((n * Hp + h) * Wp + w) * C;
+            for (int c = 0; c < C; ++c) v[(a * 2 + b) * C + c] = src[c];
+          }
+        }
+      for (int t = 0; t < 4; ++t) wd[t] = v[4 * t] | (v[4 * t + 1] << 8) | (v[4 * t + 2] << 16) | ((uint32_t)v[4 * t + 3] << 24);
+    }
+    x4[i] = make_uint4(wd[0], wd[1], wd[2], wd[3]);
   }
+}
+
+__global__ void zero_tail_kernel(uint4* p, int64_t from, int64_t to) {
+  for (int64_t i = from + threadIdx.x; i < to; i += blockDim.x) p[i] = make_uint4(0, 0, 0, 0);
 }
 
 __global__ void s2d_weight_kernel(const uint8_t* __restrict__ w, uint8_t* __restrict__ w4, int K, int R, int S, int C,
@@ -250,6 +274,11 @@ Status s2d_stem(const Problem& pb, const void* x, const void* w, void* x4, void*
   tzcdev::s2d_data_kernel<<<blocks_for(npix4), 256, 0, st>>>((const uint8_t*)x, (uint4*)x4, npix4, pb.hp, pb.wp, pb.c,
                                                              hp4, wp4);
   g_launches.fetch_add(1, std::memory_order_relaxed);
+  const int64_t padded = (npix4 + 7) / 8 * 8;
+  if (padded > npix4) {
+    tzcdev::zero_tail_kernel<<<1, 32, 0, st>>>((uint4*)x4, npix4, padded);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+  }
   const int64_t nw = (int64_t)pb.ngemm * r4 * s4 * 16;
   tzcdev::s2d_weight_kernel<<<blocks_for(nw), 256, 0, st>>>((const uint8_t*)w, (uint8_t*)w4, pb.ngemm, pb.r, pb.s, pb.c,
                                                             pb.w_stride_k, pb.w_stride_tap, r4, s4);

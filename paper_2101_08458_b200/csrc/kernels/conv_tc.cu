@@ -24,6 +24,10 @@
 #include "conv_tc.cuh"
 #include "conv_ws.cuh"
 
+#ifdef TZC_TRACE
+int g_debug_flags = 0;  // tools/trace_ws only
+#endif
+
 namespace tzcb200 {
 
 using tzcdev::ConvCfg;
@@ -332,10 +336,28 @@ void fill_epilogue(ConvKernelParams* pp, const Problem& pb, const void* seed, vo
 
 namespace {
 
+// A super-tile TMA geometry: boxes of <= 256 rows.  Pair mode reads the
+// 16-byte pixels as 128-byte rows of 8 pixels (8x fewer TMA requests; the
+// SMEM bytes are the same dense pixel array).
+void ws_boxes(const WsPlan& w, int* nbox, int* box_rows, int* box_bytes, int* div) {
+  if (w.pair) {
+    *div = 8;
+    *box_rows = (w.sr + 7) / 8 + 1;  // +1: q0/8 alignment slack is zero (q0 % 128 == 0), keep one spare row
+    *nbox = 1;
+    *box_bytes = *box_rows * 128;
+    return;
+  }
+  *div = 1;
+  *box_rows = w.box_rows;
+  *nbox = w.sr > w.box_rows ? 2 : 1;
+  *box_bytes = w.box_rows * w.kb;
+}
+
 int ws_smem(const WsPlan& w, int taps) {
   const int b = ((taps * w.c_blocks * w.bn * w.kb + 1023) / 1024) * 1024;
-  const int a_rows = w.sr > w.box_rows ? 2 * w.box_rows : w.box_rows;
-  const int slot = ((a_rows * w.kb + 1023) / 1024) * 1024;
+  int nbox, rows, bytes, div;
+  ws_boxes(w, &nbox, &rows, &bytes, &div);
+  const int slot = ((nbox * bytes + 1023) / 1024) * 1024;
   return 1024 + b + w.a_slots * slot + 256;
 }
 
@@ -402,6 +424,7 @@ bool ws_plan(const Problem& pb, bool pair, WsPlan* w) {
     if (!x.kb) return false;
   }
   x.c_blocks = (int)(cb / x.kb);
+  if ((pair ? pb.taps / 2 : pb.taps * (x.kb / 32)) > 64) return false;  // ConvKernelParams::mma_a capacity
   if ((int64_t)pb.taps * x.c_blocks * x.bn * x.kb > 160 * 1024) return false;  // weights must stay resident
   x.sr = 128 + (pb.r - 1) * pb.wp + (pb.s - 1);
   if (x.sr > 512) return false;
@@ -409,7 +432,7 @@ bool ws_plan(const Problem& pb, bool pair, WsPlan* w) {
   // padded-grid waste: (Hp*Wp)/(OH*OW) extra MMA rows
   if ((double)pb.hp * pb.wp > 1.35 * (double)pb.oh * pb.ow) return false;
   x.p_rows = (int64_t)pb.n * pb.hp * pb.wp;
-  if (x.p_rows > INT32_MAX - 1024) return false;
+  if (x.p_rows + 128 >= (int64_t(1) << 22) || (int64_t)pb.hp * pb.wp >= (1 << 18)) return false;  // exact magic division
   for (x.a_slots = 6; x.a_slots >= 2; --x.a_slots)
     if (ws_smem(x, pb.taps) <= 227 * 1024) break;
   if (x.a_slots < 2) return false;
@@ -431,10 +454,18 @@ Status run_ws(const Problem& pb, const WsPlan& w, const void* a, const void* b, 
   ConvKernelParams p;
   std::memset(&p, 0, sizeof(p));
   Status st;
-  {  // A: the input as a [N*Hp*Wp pixel rows, C] matrix
+  int nbox, box_rows, box_bytes, div;
+  ws_boxes(w, &nbox, &box_rows, &box_bytes, &div);
+  {  // A: the input as a [N*Hp*Wp pixel rows, C] matrix (pair mode: [P/8, 128 B])
     cuuint64_t dims[2] = {(cuuint64_t)pb.c, (cuuint64_t)w.p_rows};
     cuuint64_t strides[1] = {(cuuint64_t)pb.c * e};
-    cuuint32_t box[2] = {(cuuint32_t)KE, (cuuint32_t)w.box_rows};
+    cuuint32_t box[2] = {(cuuint32_t)KE, (cuuint32_t)box_rows};
+    if (w.pair) {  // workspace is padded to a whole number of 8-pixel rows
+      dims[0] = 128;
+      dims[1] = (cuuint64_t)((w.p_rows + 7) / 8);
+      strides[0] = 128;
+      box[0] = 128;
+    }
     cuuint32_t es[2] = {1, 1};
     st = enc_check(p_encode_tiled(&p.tmA, dt, 2, const_cast<void*>(a), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
                                   sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE),
@@ -463,7 +494,31 @@ Status run_ws(const Problem& pb, const WsPlan& w, const void* a, const void* b, 
   p.OWv = pb.ow;
   p.P = (int32_t)w.p_rows;
   p.SR = w.sr;
-  p.box_rows = w.box_rows;
+  p.box_rows = box_rows;
+  p.a_nbox = nbox;
+  {  // MMA table of one channel block (kernel adds cb * b_tile to B)
+    const int b_tile = w.bn * w.kb;
+    int i = 0;
+    for (int r = 0; r < pb.r; ++r)
+      for (int s = 0; s < pb.s; s += (w.pair ? 2 : 1))
+        for (int k = 0; k < (w.pair ? 1 : w.kb / 32); ++k, ++i) {
+          if (w.pair) {
+            p.mma_a[i] = (uint32_t)(r * pb.wp + s);  // 16-byte pixels
+            p.mma_b[i] = (uint32_t)(((r * pb.s + s) * b_tile) >> 4);
+          } else {
+            p.mma_a[i] = (uint32_t)(((r * pb.wp + s) * w.kb + 32 * k) >> 4);
+            p.mma_b[i] = (uint32_t)((((r * pb.s + s) * w.c_blocks) * b_tile + 32 * k) >> 4);
+          }
+        }
+    p.n_mma = i;
+  }
+#ifdef TZC_TRACE
+  p.debug_flags = ::g_debug_flags;
+#endif
+  p.magic_hw = ((uint64_t(1) << 40) + (uint64_t)pb.hp * pb.wp - 1) / ((uint64_t)pb.hp * pb.wp);
+  p.magic_wp = ((uint64_t(1) << 40) + (uint64_t)pb.wp - 1) / (uint64_t)pb.wp;
+  p.a_box_bytes = box_bytes;
+  p.a_coord_div = div;
   p.num_tiles = w.tiles;
   p.splits = w.a_slots;  // ring depth (the kernel has no split-K)
   fill_epilogue(&p, pb, seed, out, ep);
@@ -523,7 +578,7 @@ void fill_epilogue(ConvKernelParams* pp, const Problem& pb, const void* seed, vo
     const float fr = std::frexp(ep.scale, &ex);  // scale = fr * 2^ex, fr in [0.5, 1)
     if (fr == 0.5f && ex - 1 <= 0 && ex - 1 >= -24) p.pow2_k = -(ex - 1);
   }
-  p.simple = (ep.kind == tzcdev::EP_REQUANT_I8 && p.pow2_k >= 1 && !p.range_check && seed == nullptr && p.vec_ok &&
+  p.simple = (ep.kind == tzcdev::EP_REQUANT_I8 && p.pow2_k >= 2 && !p.range_check && seed == nullptr && p.vec_ok &&
               pb.out.nb == pb.ngemm)
                  ? 1
                  : 0;
@@ -548,7 +603,7 @@ Status run_problem(const Problem& pb, const void* a, const void* b, const void* 
     if (ws_plan(q, true, &w)) {
       void* x4 = nullptr;
       void* w4 = nullptr;
-      st = workspace(1, (size_t)q.n * q.hp * q.wp * 16, &x4, stream);
+      st = workspace(1, (size_t)(((int64_t)q.n * q.hp * q.wp + 7) / 8 * 8) * 16, &x4, stream);
       if (st.ok()) st = workspace(2, (size_t)q.ngemm * q.taps * 16, &w4, stream);
       if (st.ok()) st = s2d_stem(pb, a, b, x4, w4, q.hp, q.wp, q.r, q.s, stream);
       if (st.ok()) st = run_ws(q, w, x4, w4, seed, out, ep, stream);
@@ -658,8 +713,9 @@ Status run_problem(const Problem& pb, const void* a, const void* b, const void* 
 }  // namespace tzcb200
 
 #ifdef TZC_TRACE
+extern "C" void tzc_debug_flags(int f) { g_debug_flags = f; }
 extern "C" void tzc_trace_dump(unsigned long long* out) {
   cudaDeviceSynchronize();
-  cudaMemcpyFromSymbol(out, tzcdev::g_trace, sizeof(unsigned long long) * 64);
+  cudaMemcpyFromSymbol(out, tzcdev::g_trace, sizeof(unsigned long long) * 128);
 }
 #endif

@@ -32,7 +32,7 @@
 // with -DTZC_TRACE); compiles to nothing in the library.
 #ifdef TZC_TRACE
 namespace tzcdev {
-__device__ unsigned long long g_trace[64];
+__device__ unsigned long long g_trace[128];
 }
 #define TZC_TRACE_POINT(i)                                               \
   do {                                                                   \
@@ -74,7 +74,16 @@ struct alignas(64) ConvKernelParams {
   int32_t P;                   // padded rows = N * Hp * Wp
   int32_t SR;                  // A super-tile rows = 128 + (R-1)*Wp + (S-1)
   int32_t box_rows;            // rows per A TMA box (SR split in <= 2 boxes of <= 256)
-  int32_t simple;              // requant, 2^-k (k>=1), no seed, no range check, row-major, aligned
+  int32_t a_nbox, a_box_bytes, a_coord_div;  // A boxes per super-tile, bytes per box, pixel rows per TMA row
+  int32_t simple;              // requant, 2^-k (k>=2), no seed, no range check, row-major, aligned
+  uint64_t magic_hw, magic_wp; // ceil(2^40 / (Hp*Wp)), ceil(2^40 / Wp): exact q / d for q < 2^22
+  int32_t debug_flags;         // tools only: 1 = skip epilogue body, 2 = skip epilogue stores
+  // shifted-window MMA table: per MMA of a channel block, the A start-address
+  // delta and the B offset (16-byte units).  Kernel parameters live in the
+  // constant bank, so the issuing warp reads them straight into uniform
+  // registers: no per-MMA R2UR / elect waterfall (tools/mma_rate.cu).
+  int32_t n_mma;
+  uint32_t mma_a[64], mma_b[64];
 };
 
 template <int BN, int KB>
@@ -276,7 +285,11 @@ struct EpiCfg {
 // 16-byte-aligned output.  trunc(c / 2^k) = (c + ((c >> 31) >>> (32-k))) >> k.
 template <int CW>
 __device__ __forceinline__ void epi_simple(const ConvKernelParams& p, int m, int n, const uint32_t* v) {
-  const int k = p.pow2_k;
+  // trunc(c / 2^k) for |c| < 2^24, k >= 2, spread over both integer pipes:
+  //   s = c >> 31 (ALU SHF), t = c - s*(2^k - 1) (fma-pipe IMAD),
+  //   q = mulhi(t, 2^(32-k)) == t >> k (fma-pipe IMAD.HI), pack (ALU PRMT)
+  const int32_t negmask = -(int32_t)((1u << p.pow2_k) - 1u);
+  const int32_t mul = (int32_t)(1u << (32 - p.pow2_k));
   int8_t* o = static_cast<int8_t*>(p.out) + (int64_t)m * p.out_stride_m + n;
 #pragma unroll
   for (int j = 0; j < CW / 16; ++j) {
@@ -284,7 +297,8 @@ __device__ __forceinline__ void epi_simple(const ConvKernelParams& p, int m, int
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
       const int32_t c = (int32_t)v[16 * j + i];
-      b[i] = (uint32_t)((c + (int32_t)((uint32_t)(c >> 31) >> (32 - k))) >> k);
+      const int32_t t = (c >> 31) * negmask + c;
+      b[i] = (uint32_t)__mulhi(t, mul);
     }
     uint32_t w[4];
 #pragma unroll
@@ -436,7 +450,7 @@ __global__ void __launch_bounds__(EpiCfg<BN>::THREADS, 1) conv_tc_kernel(const _
         mbar_wait(&full[stage], phase);
         tc_fence_after();
         if (lane == 0 && kb == kb0) TZC_TRACE_POINT(3);
-        if (lane == 0) {
+        {  // whole warp, warp-uniform descriptors: UTCIMMA from uniform registers
           const uint32_t a_base = smem_u32(sA + stage * Cfg::A_BYTES);
           const uint32_t b_base = smem_u32(sB + stage * Cfg::B_BYTES);
 #pragma unroll
@@ -447,13 +461,13 @@ __global__ void __launch_bounds__(EpiCfg<BN>::THREADS, 1) conv_tc_kernel(const _
               bdesc = smem_desc_mnmajor_sw128(b_base + k * 16 * 128, KE * 128);
             else
               bdesc = smem_desc_kmajor(b_base + 32 * k, KB);
-            umma<kF16>(tmem_d, adesc, bdesc, IDESC, (kb > kb0 || k > 0) ? 1u : 0u);
+            if (elect_one()) umma<kF16>(tmem_d, adesc, bdesc, IDESC, (kb > kb0 || k > 0) ? 1u : 0u);
           }
-          umma_commit(&empty[stage]);
-          if (kb == kb1 - 1) {
-            umma_commit(&tfull[acc]);
-            TZC_TRACE_POINT(4);
+          if (elect_one()) {
+            umma_commit(&empty[stage]);
+            if (kb == kb1 - 1) umma_commit(&tfull[acc]);
           }
+          if (lane == 0 && kb == kb1 - 1) TZC_TRACE_POINT(4);
         }
         __syncwarp();
         if (++stage == STAGES) {

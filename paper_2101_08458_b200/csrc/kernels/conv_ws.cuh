@@ -46,8 +46,7 @@ __global__ void __launch_bounds__(EpiCfg<BN>::THREADS, 1) conv_ws_kernel(const _
   const int c_blocks = p.c_blocks;
   const int b_tile = BN * KB;                                     // one (tap, channel block) of weights
   const int b_bytes = taps * c_blocks * b_tile;
-  const int a_rows = p.SR > p.box_rows ? 2 * p.box_rows : p.box_rows;  // rows the TMA boxes write
-  const int a_slot = ((a_rows * KB + 1023) / 1024) * 1024;
+  const int a_slot = ((p.a_nbox * p.a_box_bytes + 1023) / 1024) * 1024;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sB = smem;
@@ -62,6 +61,7 @@ __global__ void __launch_bounds__(EpiCfg<BN>::THREADS, 1) conv_ws_kernel(const _
 
   const uint32_t warp = warp_id();
   const uint32_t lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) TZC_TRACE_POINT(0);
   if (warp == 0 && lane == 0) {
     tma_prefetch(&p.tmA);
     tma_prefetch(&p.tmB);
@@ -102,12 +102,15 @@ __global__ void __launch_bounds__(EpiCfg<BN>::THREADS, 1) conv_ws_kernel(const _
       uint32_t phase = 0;
       for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
         const int q0 = tile * BM;
+        const int it = (tile - (int)blockIdx.x) / (int)gridDim.x;
         for (int cb = 0; cb < c_blocks; ++cb) {
           mbar_wait(&aempty[slot], phase ^ 1);
+          if (it < 10) TZC_TRACE_POINT(10 + 5 * it);
           uint8_t* dA = sA + slot * a_slot;
-          mbar_expect_tx(&afull[slot], a_rows * KB);
-          tma_load_2d(dA, &p.tmA, &afull[slot], cb * KE, q0);
-          if (p.SR > p.box_rows) tma_load_2d(dA + p.box_rows * KB, &p.tmA, &afull[slot], cb * KE, q0 + p.box_rows);
+          mbar_expect_tx(&afull[slot], p.a_nbox * p.a_box_bytes);
+          const int row0 = q0 / p.a_coord_div;  // pair mode: 8 pixels per 128-byte TMA row
+          tma_load_2d(dA, &p.tmA, &afull[slot], cb * KE, row0);
+          if (p.a_nbox > 1) tma_load_2d(dA + p.a_box_bytes, &p.tmA, &afull[slot], cb * KE, row0 + p.box_rows);
           if (++slot == a_slots) {
             slot = 0;
             phase ^= 1;
@@ -117,44 +120,48 @@ __global__ void __launch_bounds__(EpiCfg<BN>::THREADS, 1) conv_ws_kernel(const _
     }
   } else if (warp == 1) {
     // ===================== MMA issuer =====================
+    // The whole warp runs this loop on warp-uniform values (descriptors from
+    // the kernel-parameter table), so ptxas keeps them in uniform registers
+    // and issues UTCIMMA back to back; a lane-0 loop pays ~125 cycles per MMA
+    // in R2UR + elect waterfalls, above the 48-cycle N=64 MMA (tools/mma_rate.cu).
+    const uint32_t b_base = smem_u32(sB);
     mbar_wait(bfull, 0);
     int slot = 0;
     uint32_t phase = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
-    const uint32_t b_base = smem_u32(sB);
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
       mbar_wait(&tempty[acc], acc_phase ^ 1);
       tc_fence_after();
       const uint32_t tmem_d = tmem_base + acc * BN;
+      const int it = (tile - (int)blockIdx.x) / (int)gridDim.x;
+      if (lane == 0 && it < 10) TZC_TRACE_POINT(11 + 5 * it);
       for (int cb = 0; cb < c_blocks; ++cb) {
         mbar_wait(&afull[slot], phase);
         tc_fence_after();
-        if (lane == 0) {
+        if (lane == 0 && it < 10 && cb == 0) TZC_TRACE_POINT(12 + 5 * it);
+        {
           const uint32_t a_base = smem_u32(sA + slot * a_slot);
-          if constexpr (kPair) {
-            for (int r = 0; r < p.R; ++r)
-              for (int s = 0; s < p.S; s += 2) {
-                const uint32_t shift = (uint32_t)(r * p.Wp + s);
-                const uint64_t ad = smem_desc_none(a_base + shift * 16, 16, 128);
-                const uint64_t bd = smem_desc_none(b_base + (r * p.S + s) * b_tile, BN * 16, 128);
-                umma<kF16>(tmem_d, ad, bd, IDESC, (cb > 0 || r > 0 || s > 0) ? 1u : 0u);
-              }
-          } else {
-            for (int r = 0; r < p.R; ++r)
-              for (int s = 0; s < p.S; ++s) {
-                const uint32_t shift = (uint32_t)(r * p.Wp + s) * KB;
-                const uint32_t bt = b_base + ((r * p.S + s) * c_blocks + cb) * b_tile;
-#pragma unroll
-                for (int k = 0; k < KB / 32; ++k) {
-                  const uint64_t ad = smem_desc_kmajor(a_base + shift + 32 * k, KB);
-                  const uint64_t bd = smem_desc_kmajor(bt + 32 * k, KB);
-                  umma<kF16>(tmem_d, ad, bd, IDESC, (cb > 0 || r > 0 || s > 0 || k > 0) ? 1u : 0u);
-                }
-              }
+          const uint64_t a0 = kPair ? smem_desc_none(a_base, 16, 128) : smem_desc_kmajor(a_base, KB);
+          const uint32_t b_cb = b_base + (kPair ? 0u : (uint32_t)(cb * b_tile));
+          const uint64_t b0 = kPair ? smem_desc_none(b_cb, BN * 16, 128) : smem_desc_kmajor(b_cb, KB);
+          const int n_mma = p.n_mma;
+#ifdef TZC_TRACE
+          if (p.debug_flags & 12) {
+            for (int i = 0; i < n_mma; ++i)
+              if (elect_one())
+                umma<kF16>(tmem_d, a0 + ((p.debug_flags & 4) ? 0 : p.mma_a[i]), b0 + ((p.debug_flags & 8) ? 0 : p.mma_b[i]),
+                           IDESC, (cb > 0 || i > 0) ? 1u : 0u);
+          } else
+#endif
+#pragma unroll 2
+          for (int i = 0; i < n_mma; ++i)
+            if (elect_one()) umma<kF16>(tmem_d, a0 + p.mma_a[i], b0 + p.mma_b[i], IDESC, (cb > 0 || i > 0) ? 1u : 0u);
+          if (elect_one()) {
+            umma_commit(&aempty[slot]);
+            if (cb == c_blocks - 1) umma_commit(&tfull[acc]);
           }
-          umma_commit(&aempty[slot]);
-          if (cb == c_blocks - 1) umma_commit(&tfull[acc]);
+          if (lane == 0 && it < 10 && cb == c_blocks - 1) TZC_TRACE_POINT(70 + it);
         }
         __syncwarp();
         if (++slot == a_slots) {
@@ -178,23 +185,26 @@ __global__ void __launch_bounds__(EpiCfg<BN>::THREADS, 1) conv_ws_kernel(const _
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
       const int q = tile * BM + q4 * 32 + lane;
       int m = -1;
-      if (q < p.P) {
-        const int n = q / hw, rem = q - n * hw;
-        const int oh = rem / p.Wp, ow = rem - oh * p.Wp;
+      if (q < p.P) {  // exact magic-number division (q < 2^22 host-checked)
+        const int n = (int)(((uint64_t)q * p.magic_hw) >> 40), rem = q - n * hw;
+        const int oh = (int)(((uint64_t)rem * p.magic_wp) >> 40), ow = rem - oh * p.Wp;
         if (oh < p.OH && ow < p.OWv) m = (n * p.OH + oh) * p.OWv + ow;
       }
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      {
+      const int it = (tile - (int)blockIdx.x) / (int)gridDim.x;
+      if (threadIdx.x == 128 && it < 10) TZC_TRACE_POINT(13 + 5 * it);
+      if (!(p.debug_flags & 1)) {
         constexpr int CW = EpiCfg<BN>::CW;
         const bool fast = p.vec_ok && BN <= p.Ngemm;
 #pragma unroll 1
         for (int c = 0; c < COLS / CW; ++c)
-          epi_chunk<CW, kF16, kEpm>(p, tmem_base + ((q4 * 32) << 16) + acc * BN + h * COLS + c * CW, m,
-                                    h * COLS + c * CW, fast);
+          epi_chunk<CW, kF16, kEpm>(p, tmem_base + ((q4 * 32) << 16) + acc * BN + h * COLS + c * CW,
+                                    (p.debug_flags & 2) ? -1 : m, h * COLS + c * CW, fast);
       }
       tc_fence_before();
       __syncwarp();
+      if (threadIdx.x == 128 && it < 10) TZC_TRACE_POINT(14 + 5 * it);
       if (lane == 0) mbar_arrive(&tempty[acc]);
       if (++acc == 2) {
         acc = 0;

@@ -95,7 +95,9 @@ def test_plans_for_resnet_layers(layer):
     p = D.plan_conv(d)
     assert p["bm"] == 128 and p["bn"] in (64, 128, 256) and L.k % p["bn"] == 0
     assert p["bk_bytes"] in (64, 128) and (L.c % p["bk_bytes"] == 0)
-    assert p["a_mode"] == (0 if (L.r == 1 and L.stride == 1) else 1)
+    # 0: tiled GEMM (1x1 s1), 1: TMA im2col, 2: shifted-window weight-stationary (3x3 s1, small weights)
+    want = 0 if (L.r == 1 and L.stride == 1) else (2 if layer in ("c2_3x3_64",) else 1)
+    assert p["a_mode"] == want
     assert 1 <= p["grid"] <= 148 and p["smem_bytes"] <= 227 * 1024
     assert p["splits"] >= 1 and (p["workspace_bytes"] > 0) == (p["splits"] > 1)
 
@@ -105,3 +107,11 @@ def test_plan_gemm_4096():
     d.out = D.nhwc_layout(4096)
     p = D.plan_gemm(d)
     assert (p["tiles_m"], p["tiles_n"], p["splits"]) == (32, 16, 1)
+
+
+def test_plan_stem_space_to_depth():
+    from paper_2101_08458_b200.workloads import RESNET50_V15
+    L = RESNET50_V15[0]
+    d, _ = D.conv_desc((256, L.h, L.h, L.c), (L.k, L.r, L.r, L.c), L.stride)
+    p = D.plan_conv(d)
+    assert p["a_mode"] == 3 and p["bk_bytes"] == 16 and p["bn"] == 64

@@ -123,7 +123,69 @@ __global__ void __launch_bounds__(128, 1) probe16(const uint8_t* gA, const int8_
   }
 }
 
+// MMA throughput: issue `iters` MMAs (M=128, N=NB, K=32 i8) back to back on
+// one SM; A start shifted by `shift` rows of `kb` bytes; swz: 128/64/0(none).
+template <int NB>
+__global__ void __launch_bounds__(128, 1) mma_rate(int shift, int kb, int swz, int iters, long long* cycles) {
+  extern __shared__ uint8_t raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
+  __shared__ uint64_t mbar;
+  __shared__ uint32_t slot;
+  const uint32_t warp = threadIdx.x / 32;
+  if (threadIdx.x == 0) {
+    mbar_init(&mbar, 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<256>(&slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = slot;
+  if (threadIdx.x == 0) {
+    const uint32_t a0 = smem_u32(sm) + shift * kb;
+    const uint32_t b0 = smem_u32(sm) + 64 * 1024;
+    uint64_t ad, bd;
+    if (swz == 0) {
+      ad = 0; bd = 0;
+      ad |= (uint64_t)((a0 >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)8 << 32) | ((uint64_t)1 << 46);
+      bd |= (uint64_t)((b0 >> 4) & 0x3FFF) | ((uint64_t)((NB * 16) >> 4) << 16) | ((uint64_t)8 << 32) | ((uint64_t)1 << 46);
+    } else {
+      ad = smem_desc_kmajor(a0, swz);
+      bd = smem_desc_kmajor(b0, swz);
+    }
+    long long t0 = clock64();
+    for (int i = 0; i < iters; ++i) umma<false>(tmem, ad, bd, idesc_i8(128, NB), i > 0);
+    umma_commit(&mbar);
+    mbar_wait(&mbar, 0);
+    cycles[0] = clock64() - t0;
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<256>(tmem);
+  }
+}
+
 int main() {
+  {
+    long long* dc;
+    cudaMalloc(&dc, 8);
+    auto run = [&](auto kern, const char* name, int shift, int kb, int swz) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      kern<<<1, 128, 200 * 1024>>>(shift, kb, swz, 2000, dc);
+      cudaDeviceSynchronize();
+      long long c;
+      cudaMemcpy(&c, dc, 8, cudaMemcpyDeviceToHost);
+      printf("%-12s shift %3d kb %3d swz %3d: %.1f cycles/MMA\n", name, shift, kb, swz, c / 2000.0);
+    };
+    for (int sh : {0, 1, 3, 8}) {
+      run(mma_rate<64>, "N=64", sh, 128, 128);
+      run(mma_rate<128>, "N=128", sh, 128, 128);
+      run(mma_rate<256>, "N=256", sh, 128, 128);
+      run(mma_rate<64>, "N=64 sw64", sh, 64, 64);
+      run(mma_rate<64>, "N=64 none", sh, 16, 0);
+    }
+  }
   cudaDriverEntryPointQueryResult q;
   void* fn = nullptr;
   cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &fn, 12000, cudaEnableDefault, &q);

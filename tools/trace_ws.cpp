@@ -1,0 +1,49 @@
+// Cycle trace of the shifted-window kernel, CTA 0, first 10 tiles:
+// [producer A issued, MMA tile start, MMA first A ready, epi start, epi end]
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstdlib>
+
+#include "tzc_b200.h"
+
+extern "C" void tzc_trace_dump(unsigned long long* out);
+extern "C" void tzc_debug_flags(int f);
+
+int main(int argc, char** argv) {
+  int n = argc > 1 ? atoi(argv[1]) : 256, hp = argc > 2 ? atoi(argv[2]) : 230, c = argc > 3 ? atoi(argv[3]) : 3;
+  int k = argc > 4 ? atoi(argv[4]) : 64, r = argc > 5 ? atoi(argv[5]) : 7, st = argc > 6 ? atoi(argv[6]) : 2;
+  void *x, *w, *o;
+  size_t xb = (size_t)n * hp * hp * c, wb = (size_t)k * r * r * c;
+  int oh = (hp - r) / st + 1;
+  cudaMalloc(&x, xb);
+  cudaMalloc(&w, wb);
+  cudaMalloc(&o, (size_t)n * oh * oh * k);
+  cudaMemset(x, 1, xb);
+  cudaMemset(w, 1, wb);
+  tzc_conv_desc d{};
+  d.profile = TZC_PROFILE_U8I8;
+  d.n = n; d.hp = hp; d.wp = hp; d.c = c; d.k = k; d.r = r; d.s = r; d.stride = st;
+  d.w_stride_k = (int64_t)r * r * c; d.w_stride_tap = c;
+  d.out.nb = k; d.out.stride_m = k;
+  tzc_epilogue ep{TZC_EP_REQUANT_I8, 1.0f / 4096};
+  if (argc > 7) tzc_debug_flags(atoi(argv[7]));
+  for (int it = 0; it < 3; ++it) {
+    cudaEvent_t a, b;
+    cudaEventCreate(&a); cudaEventCreate(&b);
+    cudaEventRecord(a);
+    int rc = tzc_b200_conv2d_i8(&d, (const uint8_t*)x, (const int8_t*)w, nullptr, o, &ep, nullptr);
+    cudaEventRecord(b);
+    if (rc) { printf("rc=%d %s\n", rc, tzc_b200_last_error()); return 1; }
+    cudaEventSynchronize(b);
+    float ms; cudaEventElapsedTime(&ms, a, b);
+    unsigned long long t[128];
+    tzc_trace_dump(t);
+    printf("iter %d: %.1f us total\n", it, ms * 1000);
+    for (int i = 0; i < 10; ++i)
+      printf("  tile %d: prodA=%lld mmaStart=%lld aReady=%lld issued=%lld epiStart=%lld epiEnd=%lld\n", i, (long long)(t[10 + 5 * i] - t[0]),
+             (long long)(t[11 + 5 * i] - t[0]), (long long)(t[12 + 5 * i] - t[0]), (long long)(t[70 + i] - t[0]), (long long)(t[13 + 5 * i] - t[0]),
+             (long long)(t[14 + 5 * i] - t[0]));
+  }
+  return 0;
+}
