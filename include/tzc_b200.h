@@ -151,7 +151,9 @@ TZC_API int tzc_b200_plan_gemm(const tzc_gemm_desc* d, tzc_plan* plan);
 TZC_API int tzc_b200_set_splits(int32_t splits);
 /* Process-wide options: "splits" (as above), "shifted_window" (1 = use the
  * weight-stationary shifted-window kernel for eligible stride-1 convs, the
- * default; 0 = always TMA im2col). */
+ * default; 0 = always TMA im2col), "tma_store" (1 = int8 requant outputs are
+ * staged in shared memory and written by TMA, the default; 0 = direct
+ * per-thread stores). */
 TZC_API int tzc_b200_set_option(const char* name, int64_t value);
 
 /* K5 layout adapter for the reference's channel-blocked conv2d_tdsl layouts

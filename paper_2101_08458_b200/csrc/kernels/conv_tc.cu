@@ -28,6 +28,23 @@
 int g_debug_flags = 0;  // tools/trace_ws only
 #endif
 
+namespace {
+#ifdef TZC_TRACE
+constexpr int kStaticSmem = 1024;  // s_trace
+#else
+constexpr int kStaticSmem = 0;
+#endif
+tzcdev::FastDiv make_fdiv(int64_t d) {
+  tzcdev::FastDiv f{};
+  f.d = (uint32_t)d;
+  if (d > 1) {  // m = ceil(2^64 / d)
+    const unsigned __int128 one = (unsigned __int128)1 << 64;
+    f.m = (uint64_t)((one + (unsigned __int128)d - 1) / (unsigned __int128)d);
+  }
+  return f;
+}
+}  // namespace
+
 namespace tzcb200 {
 
 using tzcdev::ConvCfg;
@@ -201,6 +218,7 @@ struct Scratch {
   size_t bytes[3] = {0, 0, 0};
 };
 std::map<cudaStream_t, Scratch> g_ws;
+int g_tma_store = 1;  // TMA-store int8 epilogue (set_option "tma_store")
 int g_forced_splits = 0;
 int g_ws_enabled = 1;  // shifted-window kernel for eligible stride-1 convs (TZC_B200_NO_WS=1 disables)
 
@@ -223,6 +241,7 @@ Status workspace(int slot, size_t bytes, void** out, cudaStream_t stream) {
 
 void set_forced_splits(int s) { g_forced_splits = s; }
 void set_ws_enabled(int on) { g_ws_enabled = on; }
+void set_tma_store(int on) { g_tma_store = on; }
 
 // ---- K7 (thin-channel) rewrite ------------------------------------------------
 bool needs_k7(const Problem& pb) { return pb.b_kn == 0 && ((int64_t)pb.c * (pb.f16 ? 2 : 1)) % 16 != 0; }
@@ -366,9 +385,9 @@ Status launch_ws_kernel(const ConvKernelParams& p, int grid, int smem, cudaStrea
   auto kern = tzcdev::conv_ws_kernel<BN, KB, F16, PAIR, EPM>;
   static int attr_smem = 0;
   if (attr_smem < smem) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024 - kStaticSmem);
     if (e != cudaSuccess) return Status(TZC_E_DEVICE, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
-    attr_smem = 227 * 1024;
+    attr_smem = 227 * 1024 - kStaticSmem;
   }
   cudaError_t e = launch_pdl(kern, dim3(grid), dim3(tzcdev::EpiCfg<BN>::THREADS), smem, stream, p);
   g_launches.fetch_add(1, std::memory_order_relaxed);
@@ -434,7 +453,7 @@ bool ws_plan(const Problem& pb, bool pair, WsPlan* w) {
   x.p_rows = (int64_t)pb.n * pb.hp * pb.wp;
   if (x.p_rows + 128 >= (int64_t(1) << 22) || (int64_t)pb.hp * pb.wp >= (1 << 18)) return false;  // exact magic division
   for (x.a_slots = 6; x.a_slots >= 2; --x.a_slots)
-    if (ws_smem(x, pb.taps) <= 227 * 1024) break;
+    if (ws_smem(x, pb.taps) <= 227 * 1024 - kStaticSmem) break;
   if (x.a_slots < 2) return false;
   x.smem = ws_smem(x, pb.taps);
   x.tiles = (int)((x.p_rows + 127) / 128);
@@ -638,6 +657,9 @@ Status run_problem(const Problem& pb, const void* a, const void* b, const void* 
 
   ConvKernelParams p;
   std::memset(&p, 0, sizeof(p));
+#ifdef TZC_TRACE
+  p.debug_flags = ::g_debug_flags;
+#endif
   // ---- A operand
   if (pb.a_mode == tzcdev::A_TILED) {
     cuuint64_t dims[2] = {(cuuint64_t)pb.a_kdim, (cuuint64_t)pb.a_rows};
@@ -701,7 +723,29 @@ Status run_problem(const Problem& pb, const void* a, const void* b, const void* 
   p.tiles_n = plan.tiles_n;
   p.num_tiles = plan.tiles_m * plan.tiles_n;
   p.splits = plan.splits;
+  p.fd_splits = make_fdiv(plan.splits);
+  p.fd_tiles_n = make_fdiv(plan.tiles_n);
+  p.fd_ohow = make_fdiv(std::max<int64_t>(1, (int64_t)pb.oh * pb.ow));
+  p.fd_ow = make_fdiv(std::max(1, pb.ow));
+  p.fd_cblocks = make_fdiv(std::max(1, p.c_blocks));
+  p.fd_s = make_fdiv(std::max(1, pb.s));
   fill_epilogue(&p, pb, seed, out, ep);
+  if (ep.kind == tzcdev::EP_REQUANT_I8 && plan.splits == 1 && p.vec_ok && pb.out.nb == pb.ngemm &&
+      pb.out.stride_m == pb.ngemm && pb.ngemm % plan.bn == 0 && g_tma_store) {
+    // int8 output as a [M, Ngemm] map; one box = 32 rows x min(BN, 128) bytes
+    const int rb = std::min(plan.bn, 128);
+    cuuint64_t dims[2] = {(cuuint64_t)pb.ngemm, (cuuint64_t)pb.m};
+    cuuint64_t strides[1] = {(cuuint64_t)pb.out.stride_m};
+    cuuint32_t box[2] = {(cuuint32_t)rb, 32};
+    cuuint32_t es[2] = {1, 1};
+    st = enc_check(p_encode_tiled(&p.tmO, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, out, dims, strides, box, es,
+                                  CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                  rb == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+                                  CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE),
+                   "cuTensorMapEncodeTiled(out)");
+    if (!st.ok()) return st;
+    p.tma_store = 1;
+  }
   if (plan.splits > 1) {
     st = workspace(0, (size_t)plan.workspace_bytes, &p.partial, stream);
     if (!st.ok()) return st;

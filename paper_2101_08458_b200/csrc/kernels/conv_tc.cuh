@@ -34,13 +34,38 @@
 namespace tzcdev {
 __device__ unsigned long long g_trace[128];
 }
-#define TZC_TRACE_POINT(i)                                               \
-  do {                                                                   \
-    if (blockIdx.x == 0) tzcdev::g_trace[(i)] = clock64();               \
+// recorded in shared memory (no global stores perturbing the timeline),
+// copied out by thread 0 of CTA 0 at kernel end
+#define TZC_TRACE_DECL __shared__ unsigned long long s_trace[128];
+#define TZC_TRACE_INIT                                  \
+  do {                                                  \
+    if (threadIdx.x < 128) s_trace[threadIdx.x] = 0ull; \
+  } while (0)
+#define TZC_TRACE_POINT(i)                                 \
+  do {                                                     \
+    if (blockIdx.x == 0) s_trace[(i)] = clock64();         \
+  } while (0)
+#define TZC_TRACE_MAX(i)                                                     \
+  do {                                                                       \
+    if (blockIdx.x == 0) atomicMax(&s_trace[(i)], (unsigned long long)clock64()); \
+  } while (0)
+#define TZC_TRACE_FLUSH                                                         \
+  do {                                                                          \
+    if (blockIdx.x == 0 && threadIdx.x < 128) tzcdev::g_trace[threadIdx.x] = s_trace[threadIdx.x]; \
   } while (0)
 #else
+#define TZC_TRACE_DECL
+#define TZC_TRACE_INIT \
+  do {                 \
+  } while (0)
 #define TZC_TRACE_POINT(i) \
   do {                     \
+  } while (0)
+#define TZC_TRACE_MAX(i) \
+  do {                   \
+  } while (0)
+#define TZC_TRACE_FLUSH \
+  do {                  \
   } while (0)
 #endif
 
@@ -49,9 +74,23 @@ namespace tzcdev {
 enum EpKind : int32_t { EP_I32 = 0, EP_REQUANT_I8 = 1, EP_F32 = 2, EP_CAST_F16 = 3, EP_PARTIAL = 4 };
 enum AMode : int32_t { A_TILED = 0, A_IM2COL = 1 };
 
+// n / d for 32-bit unsigned n by a runtime-constant d: q = umulhi64(n, m)
+// with m = ceil(2^64 / d) is exact for all n, d < 2^32 (the error term
+// n * (m*d - 2^64) / (d * 2^64) < 1/d); d == 1 is stored as m == 0.  A few
+// IMADs instead of the I2F/MUFU.RCP/F2I division sequence, whose latency
+// chain made the single-thread producer / MMA loops the per-tile bottleneck.
+struct FastDiv {
+  uint64_t m;
+  uint32_t d, pad_;
+};
+__device__ __forceinline__ uint32_t fdiv(uint32_t n, const FastDiv& f) {
+  return f.m ? (uint32_t)__umul64hi((uint64_t)n, f.m) : n;
+}
+
 struct alignas(64) ConvKernelParams {
   CUtensorMap tmA;
   CUtensorMap tmB;
+  CUtensorMap tmO;  // int8 output for the TMA-store epilogue (tma_store != 0)
   int32_t M, Ngemm;
   int32_t num_kb;    // K blocks of a full reduction
   int32_t c_blocks;  // K blocks per filter tap
@@ -76,6 +115,7 @@ struct alignas(64) ConvKernelParams {
   int32_t box_rows;            // rows per A TMA box (SR split in <= 2 boxes of <= 256)
   int32_t a_nbox, a_box_bytes, a_coord_div;  // A boxes per super-tile, bytes per box, pixel rows per TMA row
   int32_t simple;              // requant, 2^-k (k>=2), no seed, no range check, row-major, aligned
+  int32_t tma_store;           // int8 tile staged in SMEM, written by TMA (full-line stores)
   uint64_t magic_hw, magic_wp; // ceil(2^40 / (Hp*Wp)), ceil(2^40 / Wp): exact q / d for q < 2^22
   int32_t debug_flags;         // tools only: 1 = skip epilogue body, 2 = skip epilogue stores
   // shifted-window MMA table: per MMA of a channel block, the A start-address
@@ -84,6 +124,8 @@ struct alignas(64) ConvKernelParams {
   // registers: no per-MMA R2UR / elect waterfall (tools/mma_rate.cu).
   int32_t n_mma;
   uint32_t mma_a[64], mma_b[64];
+  // divisors of the general kernel's per-tile index math
+  FastDiv fd_splits, fd_tiles_n, fd_ohow, fd_ow, fd_cblocks, fd_s;
 };
 
 template <int BN, int KB>
@@ -92,10 +134,12 @@ struct ConvCfg {
   static constexpr int A_BYTES = BM * KB;
   static constexpr int B_BYTES = BN * KB;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES_RAW = (200 * 1024) / STAGE_BYTES;
+  static constexpr int STAGES_RAW = (192 * 1024) / STAGE_BYTES;
   static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
   static constexpr uint32_t TMEM_COLS = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128 : (2 * BN <= 256) ? 256 : 512;
-  static constexpr int SMEM_BYTES = 1024 /*align slack*/ + STAGES * STAGE_BYTES + 256;
+  // int8 output tile staged for the TMA store: 4 lane quarters x 32 rows x BN
+  static constexpr int STAGING_BYTES = 128 * BN;
+  static constexpr int SMEM_BYTES = 1024 /*align slack*/ + STAGING_BYTES + STAGES * STAGE_BYTES + 256;
 };
 
 // ---- epilogue math (bit-exact restatement of the reference semantics) ----
@@ -160,9 +204,21 @@ __device__ __forceinline__ uint32_t rne24(uint32_t a) {
   return (base + up) << d;
 }
 
+// TMA-store staging: one lane quarter's 32 rows x BN int8 outputs as
+// BN/RB boxes of 32 rows x RB bytes (RB = min(BN, 128)) in the TMA swizzle
+// layout of the output map (SWIZZLE_64B / 128B: 16-byte granule g of row r
+// at g ^ f(r)), so a warp's 32 rows x 16 B writes are bank-conflict free.
+template <int BN>
+__device__ __forceinline__ uint32_t stage_addr(uint32_t base, int row, int col) {
+  constexpr int RB = BN < 128 ? BN : 128;
+  const int box = col / RB, g = (col % RB) >> 4;
+  const int f = RB == 128 ? (row & 7) : ((row >> 1) & 3);
+  return base + box * (32 * RB) + row * RB + ((g ^ f) << 4);
+}
+
 // Epilogue of 16 consecutive accumulator columns v[0..16) of row m, column n.
 template <bool kF16, int kEpm, bool kVec>
-__device__ __forceinline__ void store16(const ConvKernelParams& p, int m, int n, const uint32_t* v) {
+__device__ __forceinline__ void store16(const ConvKernelParams& p, int m, int n, const uint32_t* v, uint32_t stg = 0) {
   const int64_t off = out_offset(p, m, n);
   // vector path: 16 columns in range and every piece 16-byte aligned (host
   // checked); otherwise element-wise (ragged channel counts, odd strides)
@@ -234,7 +290,10 @@ __device__ __forceinline__ void store16(const ConvKernelParams& p, int m, int n,
       w[j] = __byte_perm(__byte_perm(b[4 * j], b[4 * j + 1], 0x0040), __byte_perm(b[4 * j + 2], b[4 * j + 3], 0x0040),
                          0x5410);
     if constexpr (vec) {
-      st_v4(static_cast<int8_t*>(p.out) + off, w[0], w[1], w[2], w[3]);
+      if (stg)
+        st_shared_v4(stg, w[0], w[1], w[2], w[3]);
+      else
+        st_v4(static_cast<int8_t*>(p.out) + off, w[0], w[1], w[2], w[3]);
     } else {
 #pragma unroll
       for (int i = 0; i < 16; ++i)
@@ -283,8 +342,9 @@ struct EpiCfg {
 // The bench / serving case in a few instructions per element: requant by
 // 2^-k with no seed and |acc| < 2^24 guaranteed (host-checked), row-major
 // 16-byte-aligned output.  trunc(c / 2^k) = (c + ((c >> 31) >>> (32-k))) >> k.
-template <int CW>
-__device__ __forceinline__ void epi_simple(const ConvKernelParams& p, int m, int n, const uint32_t* v) {
+template <int CW, int BN>
+__device__ __forceinline__ void epi_simple(const ConvKernelParams& p, int m, int n, const uint32_t* v, uint32_t stg,
+                                           int srow, int scol) {
   // trunc(c / 2^k) for |c| < 2^24, k >= 2, spread over both integer pipes:
   //   s = c >> 31 (ALU SHF), t = c - s*(2^k - 1) (fma-pipe IMAD),
   //   q = mulhi(t, 2^(32-k)) == t >> k (fma-pipe IMAD.HI), pack (ALU PRMT)
@@ -305,13 +365,18 @@ __device__ __forceinline__ void epi_simple(const ConvKernelParams& p, int m, int
     for (int q = 0; q < 4; ++q)
       w[q] = __byte_perm(__byte_perm(b[4 * q], b[4 * q + 1], 0x0040), __byte_perm(b[4 * q + 2], b[4 * q + 3], 0x0040),
                          0x5410);
-    st_v4(o + 16 * j, w[0], w[1], w[2], w[3]);
+    if (stg)
+      st_shared_v4(stage_addr<BN>(stg, srow, scol + 16 * j), w[0], w[1], w[2], w[3]);
+    else
+      st_v4(o + 16 * j, w[0], w[1], w[2], w[3]);
   }
 }
 
 // One tcgen05.ld chunk of CW accumulator columns for row m (m < 0: no row).
-template <int CW, bool kF16, int kEpm>
-__device__ __forceinline__ void epi_chunk(const ConvKernelParams& p, uint32_t taddr, int m, int n, bool fast) {
+// stg != 0: int8 results go to the TMA staging tile (row srow, column scol of the tile)
+template <int CW, bool kF16, int kEpm, int BN>
+__device__ __forceinline__ void epi_chunk(const ConvKernelParams& p, uint32_t taddr, int m, int n, bool fast,
+                                          uint32_t stg = 0, int srow = 0, int scol = 0) {
   uint32_t v[CW];
   if constexpr (CW == 16)
     tmem_ld16(taddr, v);
@@ -321,13 +386,14 @@ __device__ __forceinline__ void epi_chunk(const ConvKernelParams& p, uint32_t ta
   if (m < 0) return;
   if constexpr (kEpm == EPM_REQUANT) {
     if (p.simple) {
-      epi_simple<CW>(p, m, n, v);
+      epi_simple<CW, BN>(p, m, n, v, stg, srow, scol);
       return;
     }
   }
   if (fast) {
 #pragma unroll
-    for (int j = 0; j < CW / 16; ++j) store16<kF16, kEpm, true>(p, m, n + 16 * j, v + 16 * j);
+    for (int j = 0; j < CW / 16; ++j)
+      store16<kF16, kEpm, true>(p, m, n + 16 * j, v + 16 * j, stg ? stage_addr<BN>(stg, srow, scol + 16 * j) : 0u);
   } else {
 #pragma unroll
     for (int j = 0; j < CW / 16; ++j)
@@ -345,9 +411,12 @@ __global__ void __launch_bounds__(EpiCfg<BN>::THREADS, 1) conv_tc_kernel(const _
   constexpr uint32_t IDESC = kF16 ? idesc_f16(BM, BN, kBMN) : idesc_i8(BM, BN);
 
   extern __shared__ uint8_t smem_raw[];
+  TZC_TRACE_DECL
+  TZC_TRACE_INIT;
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sA = smem;
-  uint8_t* sB = smem + STAGES * Cfg::A_BYTES;
+  uint8_t* sStage = smem;  // TMA-store staging (1024-aligned, STAGING_BYTES)
+  uint8_t* sA = smem + Cfg::STAGING_BYTES;
+  uint8_t* sB = sA + STAGES * Cfg::A_BYTES;
   uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * Cfg::B_BYTES);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
@@ -382,7 +451,6 @@ __global__ void __launch_bounds__(EpiCfg<BN>::THREADS, 1) conv_tc_kernel(const _
   // previous grid's writes before touching global memory
   pdl_launch_dependents();
   pdl_wait();
-  if (threadIdx.x == 0) TZC_TRACE_POINT(1);
 
   const int num_units = p.num_tiles * p.splits;
 
@@ -392,27 +460,29 @@ __global__ void __launch_bounds__(EpiCfg<BN>::THREADS, 1) conv_tc_kernel(const _
       int stage = 0;
       uint32_t phase = 0;
       for (int u = blockIdx.x; u < num_units; u += gridDim.x) {
-        const int tile = u / p.splits, split = u - tile * p.splits;
-        const int m_tile = tile / p.tiles_n, n_tile = tile - m_tile * p.tiles_n;
-        const int kb0 = (int)((int64_t)split * p.num_kb / p.splits);
-        const int kb1 = (int)((int64_t)(split + 1) * p.num_kb / p.splits);
+        const int tile = (int)fdiv(u, p.fd_splits), split = u - tile * p.splits;
+        const int m_tile = (int)fdiv(tile, p.fd_tiles_n), n_tile = tile - m_tile * p.tiles_n;
+        const int kb0 = (int)fdiv(split * p.num_kb, p.fd_splits);
+        const int kb1 = (int)fdiv((split + 1) * p.num_kb, p.fd_splits);
         const int m0 = m_tile * BM, n0 = n_tile * BN;
         int img = 0, oh = 0, ow = 0;
         if constexpr (kAMode == A_IM2COL) {
-          img = m0 / p.OHOW;
+          img = (int)fdiv(m0, p.fd_ohow);
           const int rem = m0 - img * p.OHOW;
-          oh = rem / p.OW;
+          oh = (int)fdiv(rem, p.fd_ow);
           ow = rem - oh * p.OW;
         }
+        const int it = (u - (int)blockIdx.x) / (int)gridDim.x;
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
-          const int tap = kb / p.c_blocks;
+          if (kb == kb0 && it < 10) TZC_TRACE_POINT(10 + 5 * it);
+          const int tap = (int)fdiv(kb, p.fd_cblocks);
           const int cb = kb - tap * p.c_blocks;
           uint8_t* dA = sA + stage * Cfg::A_BYTES;
           uint8_t* dB = sB + stage * Cfg::B_BYTES;
           mbar_expect_tx(&full[stage], Cfg::STAGE_BYTES);
           if constexpr (kAMode == A_IM2COL) {
-            const int r = tap / p.S, s = tap - r * p.S;
+            const int r = (int)fdiv(tap, p.fd_s), s = tap - r * p.S;
             tma_load_im2col_4d(dA, &p.tmA, &full[stage], cb * KE, ow * p.stride, oh * p.stride, img,
                                (uint16_t)s, (uint16_t)r);
           } else {
@@ -430,7 +500,6 @@ __global__ void __launch_bounds__(EpiCfg<BN>::THREADS, 1) conv_tc_kernel(const _
             phase ^= 1;
           }
         }
-        TZC_TRACE_POINT(2);
       }
     }
   } else if (warp == 1) {
@@ -440,16 +509,20 @@ __global__ void __launch_bounds__(EpiCfg<BN>::THREADS, 1) conv_tc_kernel(const _
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int u = blockIdx.x; u < num_units; u += gridDim.x) {
-      const int split = u % p.splits;
-      const int kb0 = (int)((int64_t)split * p.num_kb / p.splits);
-      const int kb1 = (int)((int64_t)(split + 1) * p.num_kb / p.splits);
+      const int it = (u - (int)blockIdx.x) / (int)gridDim.x;
+      if (lane == 0 && it < 10) TZC_TRACE_POINT(80 + it);
+      const int split = u - (int)fdiv(u, p.fd_splits) * p.splits;
+      const int kb0 = (int)fdiv(split * p.num_kb, p.fd_splits);
+      const int kb1 = (int)fdiv((split + 1) * p.num_kb, p.fd_splits);
       mbar_wait(&tempty[acc], acc_phase ^ 1);
+      if (lane == 0 && it < 10) TZC_TRACE_POINT(90 + it);
       tc_fence_after();
       const uint32_t tmem_d = tmem_base + acc * BN;
+      if (lane == 0 && it < 10) TZC_TRACE_POINT(11 + 5 * it);
       for (int kb = kb0; kb < kb1; ++kb) {
         mbar_wait(&full[stage], phase);
         tc_fence_after();
-        if (lane == 0 && kb == kb0) TZC_TRACE_POINT(3);
+        if (lane == 0 && kb == kb0 && it < 10) TZC_TRACE_POINT(12 + 5 * it);
         {  // whole warp, warp-uniform descriptors: UTCIMMA from uniform registers
           const uint32_t a_base = smem_u32(sA + stage * Cfg::A_BYTES);
           const uint32_t b_base = smem_u32(sB + stage * Cfg::B_BYTES);
@@ -467,7 +540,7 @@ __global__ void __launch_bounds__(EpiCfg<BN>::THREADS, 1) conv_tc_kernel(const _
             umma_commit(&empty[stage]);
             if (kb == kb1 - 1) umma_commit(&tfull[acc]);
           }
-          if (lane == 0 && kb == kb1 - 1) TZC_TRACE_POINT(4);
+          if (lane == 0 && kb == kb1 - 1 && it < 10) TZC_TRACE_POINT(70 + it);
         }
         __syncwarp();
         if (++stage == STAGES) {
@@ -488,16 +561,18 @@ __global__ void __launch_bounds__(EpiCfg<BN>::THREADS, 1) conv_tc_kernel(const _
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int u = blockIdx.x; u < num_units; u += gridDim.x) {
-      const int tile = u / p.splits, split = u - tile * p.splits;
-      const int m_tile = tile / p.tiles_n, n_tile = tile - m_tile * p.tiles_n;
+      const int tile = (int)fdiv(u, p.fd_splits), split = u - tile * p.splits;
+      const int m_tile = (int)fdiv(tile, p.fd_tiles_n), n_tile = tile - m_tile * p.tiles_n;
       const int m = m_tile * BM + q * 32 + lane;
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      if (threadIdx.x == 128) TZC_TRACE_POINT(5);
+      const int it = (u - (int)blockIdx.x) / (int)gridDim.x;
+      if (threadIdx.x == 128 && it < 10) TZC_TRACE_POINT(13 + 5 * it);
       // whole tile in range and 16-byte aligned: the compact vector epilogue;
       // otherwise (ragged channels, odd strides) the element-wise one
       const bool fast = p.vec_ok && (n_tile + 1) * BN <= p.Ngemm;
-      if (p.ep_kind == EP_PARTIAL) {
+      if (p.debug_flags & 1) {
+      } else if (p.ep_kind == EP_PARTIAL) {
         constexpr int CW = EpiCfg<BN>::CW;
 #pragma unroll 1
         for (int c = 0; c < HALF / CW; ++c) {
@@ -516,20 +591,42 @@ __global__ void __launch_bounds__(EpiCfg<BN>::THREADS, 1) conv_tc_kernel(const _
               if (n + 4 * j < p.Ngemm) st_v4(o + 4 * j, v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
           }
         }
+      } else if (kEpm == EPM_REQUANT && p.tma_store) {
+        // int8 tile -> SMEM staging (this lane quarter's 32 rows x BN) ->
+        // one TMA store per 128-byte column box: whole 128-byte output lines
+        // instead of 32 scattered 16-byte pieces per warp store.
+        constexpr int CW = EpiCfg<BN>::CW;
+        constexpr int RB = BN < 128 ? BN : 128;
+        uint8_t* stq = sStage + q * (32 * BN);
+        if (h == 0 && lane == 0) bulk_wait_read0();  // previous tile's store has read the staging
+        named_bar_sync(1 + q, 128);
+#pragma unroll 1
+        for (int c = 0; c < HALF / CW; ++c) {
+          const int col = h * HALF + c * CW;
+          epi_chunk<CW, kF16, kEpm, BN>(p, tmem_base + ((q * 32) << 16) + acc * BN + col,
+                                        (m < p.M && !(p.debug_flags & 2)) ? m : -1, n_tile * BN + col, true,
+                                        smem_u32(stq), (int)lane, col);
+        }
+        fence_proxy_async_smem();
+        named_bar_sync(1 + q, 128);
+        if (h == 0 && lane == 0) {
+#pragma unroll
+          for (int b = 0; b < BN / RB; ++b) tma_store_2d(&p.tmO, stq + b * (32 * RB), n_tile * BN + b * RB, m_tile * BM + q * 32);
+          bulk_commit();
+        }
       } else {
         constexpr int CW = EpiCfg<BN>::CW;
 #pragma unroll 1
         for (int c = 0; c < HALF / CW; ++c) {
           const int col = h * HALF + c * CW;
-          if (threadIdx.x == 128) TZC_TRACE_POINT(8 + 3 * c);
-          epi_chunk<CW, kF16, kEpm>(p, tmem_base + ((q * 32) << 16) + acc * BN + col, m < p.M ? m : -1,
-                                    n_tile * BN + col, fast);
-          if (threadIdx.x == 128) TZC_TRACE_POINT(10 + 3 * c);
+          epi_chunk<CW, kF16, kEpm, BN>(p, tmem_base + ((q * 32) << 16) + acc * BN + col,
+                                        (m < p.M && !(p.debug_flags & 2)) ? m : -1, n_tile * BN + col, fast);
         }
       }
       tc_fence_before();
       __syncwarp();
-      if (threadIdx.x == 128) TZC_TRACE_POINT(6);
+      if (threadIdx.x == 128 && it < 10) TZC_TRACE_POINT(14 + 5 * it);
+      if (lane == 0 && it < 10) TZC_TRACE_MAX(100 + it);
       if (lane == 0) mbar_arrive(&tempty[acc]);
       if (++acc == 2) {
         acc = 0;
@@ -537,9 +634,11 @@ __global__ void __launch_bounds__(EpiCfg<BN>::THREADS, 1) conv_tc_kernel(const _
       }
     }
   }
+  if (kEpm == EPM_REQUANT && p.tma_store && warp >= 4 && ((warp - 4) >> 2) == 0 && lane == 0)
+    bulk_wait0();  // staged stores complete before the CTA (and its SMEM) retires
   __syncwarp();  // roles diverge within warps 0/1; bar.sync requires convergence
   __syncthreads();
-  if (threadIdx.x == 0) TZC_TRACE_POINT(7);
+  TZC_TRACE_FLUSH;
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc<Cfg::TMEM_COLS>(tmem_base);

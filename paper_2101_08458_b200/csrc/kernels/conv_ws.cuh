@@ -48,6 +48,8 @@ __global__ void __launch_bounds__(EpiCfg<BN>::THREADS, 1) conv_ws_kernel(const _
   const int b_bytes = taps * c_blocks * b_tile;
   const int a_slot = ((p.a_nbox * p.a_box_bytes + 1023) / 1024) * 1024;
   extern __shared__ uint8_t smem_raw[];
+  TZC_TRACE_DECL
+  TZC_TRACE_INIT;
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sB = smem;
   uint8_t* sA = smem + ((b_bytes + 1023) / 1024) * 1024;
@@ -199,7 +201,7 @@ __global__ void __launch_bounds__(EpiCfg<BN>::THREADS, 1) conv_ws_kernel(const _
         const bool fast = p.vec_ok && BN <= p.Ngemm;
 #pragma unroll 1
         for (int c = 0; c < COLS / CW; ++c)
-          epi_chunk<CW, kF16, kEpm>(p, tmem_base + ((q4 * 32) << 16) + acc * BN + h * COLS + c * CW,
+          epi_chunk<CW, kF16, kEpm, BN>(p, tmem_base + ((q4 * 32) << 16) + acc * BN + h * COLS + c * CW,
                                     (p.debug_flags & 2) ? -1 : m, h * COLS + c * CW, fast);
       }
       tc_fence_before();
@@ -214,6 +216,7 @@ __global__ void __launch_bounds__(EpiCfg<BN>::THREADS, 1) conv_ws_kernel(const _
   }
   __syncwarp();
   __syncthreads();
+  TZC_TRACE_FLUSH;
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc<TMEM_COLS>(tmem_base);

@@ -42,6 +42,7 @@ Status run_problem(const Problem& pb, const void* a, const void* b, const void* 
                    const tzc_epilogue& ep, cudaStream_t stream);
 void set_forced_splits(int s);
 void set_ws_enabled(int on);
+void set_tma_store(int on);
 int device_ok();
 int num_sms();
 

@@ -1,0 +1,65 @@
+"""The TMA-store int8 epilogue (SMEM staging in the output map's swizzle,
+one cp.async.bulk.tensor store per lane quarter and 128-byte column box) vs
+the oracle and vs the direct-store epilogue: bit-exact, including ragged M
+(rows clipped by the map), every BN (64/128/256 -> SWIZZLE_64B/128B, one or
+two boxes), seeds (general requant path) and the simple 2^-k path."""
+import numpy as np
+import pytest
+import torch
+
+from oracle.pyoracle import Orc
+from paper_2101_08458_b200 import device as D
+from tests.gpu_helpers import to_dev
+
+pytestmark = pytest.mark.gpu
+
+
+def gemm_q(cuda, a, b, scale, seed=None, tma=True):
+    D.set_option("tma_store", 1 if tma else 0)
+    try:
+        return D.gemm(to_dev(a, cuda), to_dev(b, cuda), None if seed is None else to_dev(seed, cuda),
+                      epilogue="requant_i8", scale=scale).cpu().numpy()
+    finally:
+        D.set_option("tma_store", 1)
+
+
+@pytest.mark.parametrize("m,n,k", [(1000, 64, 64), (777, 128, 128), (1283, 256, 64), (300, 512, 256),
+                                   (128, 64, 32), (4096, 256, 128)])
+@pytest.mark.parametrize("scale", [2.0 ** -12, 0.0003])
+def test_tma_store_gemm_requant(cuda, m, n, k, scale):
+    a = Orc.random_tensor("u8", (m, k), 400)
+    b = Orc.random_tensor("i8", (n, k), 401)
+    want = Orc.requant_i8(Orc.matmul(a, b), scale)
+    assert np.array_equal(gemm_q(cuda, a, b, scale), want)
+    assert np.array_equal(gemm_q(cuda, a, b, scale, tma=False), want)
+
+
+def test_tma_store_with_seed(cuda):
+    m, n, k = 515, 128, 96
+    a = Orc.random_tensor("u8", (m, k), 410)
+    b = Orc.random_tensor("i8", (n, k), 411)
+    s0 = Orc.random_tensor("i32", (m, n), 412)
+    want = Orc.requant_i8(Orc.matmul(a, b, s0), 2.0 ** -10)
+    assert np.array_equal(gemm_q(cuda, a, b, 2.0 ** -10, seed=s0), want)
+
+
+@pytest.mark.parametrize("n,hp,c,k,r,stride", [(2, 30, 64, 256, 1, 1), (3, 17, 128, 64, 3, 2), (1, 58, 64, 128, 1, 2)])
+def test_tma_store_conv_requant(cuda, n, hp, c, k, r, stride):
+    x = Orc.random_tensor("u8", (n, hp, hp, c), 420)
+    w = Orc.random_tensor("i8", (k, r, r, c), 421)
+    scale = 2.0 ** -13
+    want = Orc.requant_i8(Orc.conv2d_nhwc(x, w, stride), scale)
+    got = D.conv2d(to_dev(x, cuda), to_dev(w, cuda), stride, epilogue="requant_i8", scale=scale).cpu().numpy()
+    assert np.array_equal(got, want)
+
+
+def test_tma_store_output_untouched_outside(cuda):
+    """Clipping: a 1000-row output inside a larger buffer; rows past M keep their bytes."""
+    m, n, k = 1000, 256, 64
+    a = Orc.random_tensor("u8", (m, k), 430)
+    b = Orc.random_tensor("i8", (n, k), 431)
+    big = torch.full((m + 200, n), 77, dtype=torch.int8, device=cuda)
+    D.gemm(to_dev(a, cuda), to_dev(b, cuda), epilogue="requant_i8", scale=2.0 ** -12, out=big[:m])
+    got = big.cpu().numpy()
+    assert np.array_equal(got[:m], Orc.requant_i8(Orc.matmul(a, b), 2.0 ** -12))
+    assert (got[m:] == 77).all()

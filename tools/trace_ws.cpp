@@ -1,4 +1,5 @@
-// Cycle trace of the shifted-window kernel, CTA 0, first 10 tiles:
+// Cycle trace of one conv launch (shifted-window or general kernel), CTA 0, first 10 tiles:
+// args: n hp c k r stride [debug_flags] [shifted_window 0/1]
 // [producer A issued, MMA tile start, MMA first A ready, epi start, epi end]
 #include <cuda_runtime.h>
 
@@ -28,6 +29,7 @@ int main(int argc, char** argv) {
   d.out.nb = k; d.out.stride_m = k;
   tzc_epilogue ep{TZC_EP_REQUANT_I8, 1.0f / 4096};
   if (argc > 7) tzc_debug_flags(atoi(argv[7]));
+  if (argc > 8) tzc_b200_set_option("shifted_window", atoi(argv[8]));
   for (int it = 0; it < 3; ++it) {
     cudaEvent_t a, b;
     cudaEventCreate(&a); cudaEventCreate(&b);
@@ -44,6 +46,9 @@ int main(int argc, char** argv) {
       printf("  tile %d: prodA=%lld mmaStart=%lld aReady=%lld issued=%lld epiStart=%lld epiEnd=%lld\n", i, (long long)(t[10 + 5 * i] - t[0]),
              (long long)(t[11 + 5 * i] - t[0]), (long long)(t[12 + 5 * i] - t[0]), (long long)(t[70 + i] - t[0]), (long long)(t[13 + 5 * i] - t[0]),
              (long long)(t[14 + 5 * i] - t[0]));
+    for (int i = 0; i < 10; ++i)
+      printf("  tile %d: mmaLoopTop=%lld temptyOk=%lld lastEpiWarpEnd=%lld\n", i, (long long)(t[80 + i] - t[0]),
+             (long long)(t[90 + i] - t[0]), (long long)(t[100 + i] - t[0]));
   }
   return 0;
 }
