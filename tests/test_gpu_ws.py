@@ -81,3 +81,24 @@ def test_ws_f16(cuda):
     w = Orc.random_tensor("fp16", (k, r, r, c), 331)
     ref = Orc.conv2d_nhwc(x, w, 1, fp16=True)
     assert rel_dev(ref, run(cuda, x, w, 1, epilogue="f32")) <= 1e-3
+
+
+@pytest.mark.parametrize("n,hp,c,k,r", WS_CASES + [(2, 9, 512, 64, 3), (5, 7, 64, 128, 3)])
+def test_ws_requant_tiny_images(cuda, n, hp, c, k, r):
+    """Requant of the padded grid, incl. tiny images (Wp < 32: one lane
+    quarter's 32-pixel run spans several image rows and images), general
+    (seeded) and 2^-k paths, with the tma_store option on and off (it must
+    never change a result)."""
+    x = Orc.random_tensor("u8", (n, hp, hp, c), 340)
+    w = Orc.random_tensor("i8", (k, r, r, c), 341)
+    o = hp - r + 1
+    s0 = Orc.random_tensor("i32", (n, o, o, k), 342)
+    for scale, seed in ((2.0 ** -13, None), (0.00071, s0)):
+        want = Orc.requant_i8(Orc.conv2d_nhwc(x, w, 1, seed), scale)
+        for tma in (1, 0):
+            D.set_option("tma_store", tma)
+            try:
+                got = run(cuda, x, w, 1, seed, epilogue="requant_i8", scale=scale)
+            finally:
+                D.set_option("tma_store", 1)
+            assert np.array_equal(got, want), (scale, tma)
