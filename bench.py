@@ -4,10 +4,11 @@
 Metric (BASELINE.json): "ResNet-50 int8 conv-layer TOPS & % tcgen05 i8 peak at
 1/2/4/8 B200".  One *step* = one pass of the 23 distinct ResNet-50 v1.5 conv
 shapes (pad materialised, valid conv over NHWC u8 x
-[K,R,S,C] i8 -> i32 accumulate -> fused requant to i8) at the per-GPU batch
-(default 32: configs[2] at N=1; N=8 ranks x 32 = configs[4]'s batch 256).
-Scaling is weak (independent images per rank, no collective on the data
-path).  ops = 2*N*OH*OW*K*C*R*S with the real C (stem C=3).
+[K,R,S,C] i8 -> i32 accumulate -> fused requant to i8) over a global batch
+of 256 images sharded over the ranks (BASELINE.json configs[4]: "batch 256
+sharded over batch at 1/2/4/8 B200"; N=1 runs all 256, N=8 runs 32 per GPU
+= configs[2]'s shape).  Scaling is strong (fixed total work); no collective
+on the data path.  ops = 2*N*OH*OW*K*C*R*S with the real C (stem C=3).
 
 Timing: W warm-up steps, then K steps, each replaying one CUDA graph of the
 23 layer launches with cudaEventRecordExternal events around every layer
@@ -44,7 +45,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--batch", type=int, default=32, help="images per GPU")
+    ap.add_argument("--batch", type=int, default=256, help="global batch, sharded over the ranks")
     ap.add_argument("--layers", default="", help="comma list of layer names (default: all 23)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -53,6 +54,28 @@ def parse():
     ap.add_argument("--branches", type=int, default=4,
                     help="parallel graph branches for the timed step (independent layers overlap tails)")
     return ap.parse_args()
+
+
+def max_over_ranks(x: float, world: int, device) -> float:
+    """The slowest rank's time: all_reduce(MAX) over the job (NCCL on GPUs, gloo in the CPU tests)."""
+    if world <= 1:
+        return float(x)
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(x)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def job_tops(ops_per_rank: int, world: int, ms_per_step: float) -> float:
+    """Whole-job throughput: every rank runs ops_per_rank per step (equal shards)."""
+    return ops_per_rank * world / (ms_per_step * 1e-3) / 1e12
+
+
+def shard_batch(global_batch: int, world: int) -> int:
+    if global_batch % world:
+        raise ValueError(f"global batch {global_batch} does not divide over {world} ranks")
+    return global_batch // world
 
 
 def dist_env():
@@ -175,9 +198,10 @@ def run_ours(args, rank, world, local):
     names = [s for s in args.layers.split(",") if s]
     gen = torch.Generator(device=dev)
     gen.manual_seed(1234 + rank)
-    layers, bufs = build_suite(torch, dev, args.batch, names, gen)
-    ops_step = sum(L.ops(args.batch) for L in layers)
-    bytes_step = sum(L.algo_bytes(args.batch) for L in layers)
+    bpg = shard_batch(args.batch, world)  # images on this rank
+    layers, bufs = build_suite(torch, dev, bpg, names, gen)
+    ops_step = sum(L.ops(bpg) for L in layers)
+    bytes_step = sum(L.algo_bytes(bpg) for L in layers)
     stream = torch.cuda.Stream(device=dev)
     flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device=dev)
     rt = Cudart()
@@ -196,7 +220,7 @@ def run_ours(args, rank, world, local):
     # parallel branches (largest first, round robin) so one layer's tail and
     # launch latency overlap the next layer's work.
     branch_streams = [torch.cuda.Stream(device=dev) for _ in range(max(1, args.branches))]
-    order = sorted(range(len(bufs)), key=lambda i: -bufs[i]["layer"].ops(args.batch))
+    order = sorted(range(len(bufs)), key=lambda i: -bufs[i]["layer"].ops(bpg))
 
     def suite_branches():
         fork = torch.cuda.Event()
@@ -271,21 +295,17 @@ def run_ours(args, rank, world, local):
         suite(False)
     torch.cuda.synchronize()
     launches_per_step = D.launch_count() - c0
-    total_ms = sum(step_ms)
-    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    total_ms = float(t.item())
+    total_ms = max_over_ranks(sum(step_ms), world, dev)
     ms_step = total_ms / args.steps
-    value = ops_step * world / (ms_step * 1e-3) / 1e12  # TOPS, whole job
+    value = job_tops(ops_step, world, ms_step)  # TOPS, whole job
 
     pk = peaks()
     layer_rows = []
     for b, v in zip(bufs, per_layer):
         L = b["layer"]
         ms = statistics.median(v)
-        ops = L.ops(args.batch)
-        by = L.algo_bytes(args.batch)
+        ops = L.ops(bpg)
+        by = L.algo_bytes(bpg)
         roof = min(SPEC_I8_TOPS, ops / by * pk["hbm_gbs"] / 1e3)
         layer_rows.append({"layer": L.name, "ms": ms, "tops": ops / (ms * 1e-3) / 1e12,
                            "gbs": by / (ms * 1e-3) / 1e9, "roofline_tops_spec": roof,
@@ -299,12 +319,12 @@ def run_ours(args, rank, world, local):
         "warmup": args.warmup,
         "ms_per_step": round(ms_step, 4),
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "strong",
         "vs_baseline": None,
         "dtype": "u8xi8->i32 (requant i8 out)",
         "data": "synthetic (uniform u8 activations / i8 weights, torch.Generator seeded per rank)",
         "config": {"workload": "resnet50_v1.5_int8_conv_suite (23 distinct shapes, SURVEY.md App. A)",
-                   "batch_per_gpu": args.batch, "global_batch": args.batch * world,
+                   "batch_per_gpu": bpg, "global_batch": args.batch,
                    "layers": len(layers), "ops_per_step_per_gpu": ops_step,
                    "algo_bytes_per_step_per_gpu": bytes_step,
                    "l2": "flushed (512 MiB memset) between timed steps, outside the timed events",
@@ -315,16 +335,34 @@ def run_ours(args, rank, world, local):
         "clocks": clk.summary(),
     }
     kern_ms = sum(statistics.median(v) for v in per_layer)  # per-layer event sum (graph B)
-    achieved = ops_step / (kern_ms * 1e-3) / 1e12
+    suite_achieved = ops_step / (kern_ms * 1e-3) / 1e12
+    # roofline of the dominant kernel: the layer with the largest share of the
+    # step; its own bound (HBM when its arithmetic intensity is below the
+    # ridge, else the int8 tensor peak); achieved = algorithmic bytes (or ops)
+    # per launch / its per-layer event time (graph B replays, same stream,
+    # same L2-flush protocol, right after the timed region)
+    dom = max(layer_rows, key=lambda r: r["ms"])
+    dL = next(L for L in layers if L.name == dom["layer"])
+    hbm_bound = dom["roofline_tops_spec"] < SPEC_I8_TOPS
+    if hbm_bound:
+        ach, peak, unit = dL.algo_bytes(bpg) / (dom["ms"] * 1e-3) / 1e9, pk["hbm_gbs"], "GB/s"
+    else:
+        ach, peak, unit = dom["tops"], pk["i8_tops"], "TFLOP/s"
     result["roofline"] = {
-        "bound": "tensor", "kernel": "conv_tc_kernel (tcgen05 kind::i8, all 23 layers)",
-        "achieved": round(achieved, 2), "peak": round(pk["i8_tops"], 1), "unit": "TFLOP/s",
-        "frac": round(achieved / pk["i8_tops"], 4),
-        "peak_basis": f"2 x bf16 burst, {pk['source']}; spec dense i8 = {SPEC_I8_TOPS}",
-        "frac_of_spec": round(achieved / SPEC_I8_TOPS, 4),
-        "suite_cold_hbm_ceiling_frac_of_spec": round(
-            ops_step / sum(L.ops(args.batch) / r["roofline_tops_spec"] for L, r in zip(layers, layer_rows)) / SPEC_I8_TOPS, 4),
-        "traffic": traffic_from_profiles(),
+        "bound": "hbm" if hbm_bound else "tensor",
+        "kernel": f"{dom['layer']} ({kernel_name(dom.get('plan', {}))})",
+        "achieved": round(ach, 2), "peak": round(peak, 1), "unit": unit, "frac": round(ach / peak, 4),
+        "peak_basis": (f"HBM copy bandwidth, {pk['source']}" if hbm_bound else
+                       f"2 x bf16 burst, {pk['source']}; spec dense i8 = {SPEC_I8_TOPS}"),
+        "algorithmic_per_launch": {"bytes": dL.algo_bytes(bpg), "ops": dL.ops(bpg)},
+        "share_of_step": round(dom["ms"] / kern_ms, 4),
+        "traffic": traffic_from_profiles(dom["layer"]),
+        "suite": {"bound": "tensor", "achieved": round(suite_achieved, 2), "peak": round(pk["i8_tops"], 1),
+                  "unit": "TFLOP/s", "frac": round(suite_achieved / pk["i8_tops"], 4),
+                  "frac_of_spec": round(suite_achieved / SPEC_I8_TOPS, 4),
+                  "cold_hbm_ceiling_frac_of_spec": round(
+                      ops_step / sum(L.ops(bpg) / r["roofline_tops_spec"] for L, r in zip(layers, layer_rows))
+                      / SPEC_I8_TOPS, 4)},
     }
     if not args.no_e2e:
         result["e2e"] = run_e2e(args, torch, D, bufs, stream, ops_step, world, dist)
@@ -348,11 +386,22 @@ def plan_of(D, b):
         return {"error": str(e)}
 
 
-def traffic_from_profiles():
+def kernel_name(plan):
+    if not plan or "a_mode" not in plan:
+        return "conv kernel"
+    mode = {0: "conv_tc_kernel tiled", 1: "conv_tc_kernel TMA-im2col", 2: "conv_ws_kernel shifted-window",
+            3: "s2d + conv_ws_kernel pair"}.get(plan["a_mode"], "conv kernel")
+    return f"{mode}, BN={plan['bn']}, tcgen05 kind::i8"
+
+
+def traffic_from_profiles(layer):
+    """DRAM read+write bytes per launch of this layer's kernel from the committed ncu capture, or None."""
     p = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(p):
         with open(p) as f:
-            return json.load(f).get("dram_bytes_per_step")
+            ent = json.load(f).get("layers", {}).get(layer)
+        if ent:
+            return ent["dram_bytes_per_launch"]
     return None
 
 
@@ -392,12 +441,8 @@ def run_e2e(args, torch, D, bufs, stream, ops_step, world, dist):
     for _ in range(steps):
         step()
     torch.cuda.synchronize()
-    ms = (time.perf_counter() - t0) * 1e3
-    t = torch.tensor([ms], dtype=torch.float64, device=stream.device)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms = float(t.item()) / steps
-    return {"value": round(ops_step * world / (ms * 1e-3) / 1e12, 3), "unit": "TOPS",
+    ms = max_over_ranks((time.perf_counter() - t0) * 1e3, world, stream.device) / steps
+    return {"value": round(job_tops(ops_step, world, ms), 3), "unit": "TOPS",
             "ms_per_step": round(ms, 3), "steps": steps,
             "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
             "path": "tzc_b200_run_op (op text + tcgen05 instruction + pinned host buffers + fused requant op), "
@@ -473,10 +518,13 @@ def run_reference(args, rank, world):
     value = 2 * tot_macs / tot_s / 1e12
     res = {"metric": METRIC, "value": round(value, 9), "unit": "TOPS", "impl": "reference", "n_gpus": world,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * tot_s / args.steps, 2),
-           "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+           "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
            "dtype": "u8xi8->i32", "data": "synthetic (reference random_inputs, seed 0)",
-           "config": {"workload": "resnet50_v1.5_int8_conv_suite (bounded per-layer slices)",
-                      "batch_per_gpu": args.batch, "layers": len(layers)},
+           "config": {"workload": "resnet50_v1.5_int8_conv_suite (23 distinct shapes, SURVEY.md App. A)",
+                      "global_batch": args.batch, "batch_per_gpu": args.batch // max(1, world),
+                      "layers": len(layers),
+                      "timed_sample": "bounded per-layer slices (1 image x 1 output row x K' channels); "
+                                      "TOPS = sample MACs x 2 / sample seconds"},
            "cpu_baseline": {"value": round(value, 9), "unit": "TOPS", "cores": threads, "kind": "reference",
                             "sample": f"per step: 1 image x 1 output row x K' channels of each of {len(layers)} "
                                       f"layers ({sum(i[2] for i in items)} MAC); eval_tir(vdot_16x4), "

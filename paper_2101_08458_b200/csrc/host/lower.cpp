@@ -512,19 +512,113 @@ void run_tensorized_packed(const TensorizedOp& t, const std::map<std::string, co
     hs = it == host.end() ? nullptr : it->second;  // absent initial image => zeros
   }
   std::lock_guard<std::mutex> lk(g_pool_mu);
-  cudaStream_t st = nullptr;
   const size_t xb = td.size() * elem_bytes(td.dtype), wb = tw.size() * elem_bytes(tw.dtype);
   const size_t sb = to.size() * elem_bytes(to.dtype);
   void* dx = pool(0, xb);
   void* dw = pool(1, wb);
   void* ds = hs ? pool(2, sb) : nullptr;
   void* dout = pool(3, (size_t)out_bytes);
+  tzc_out_layout ol{};
+  ol.nb = (int32_t)p.out_nb;
+  ol.stride_m = p.out_stride_m;
+  ol.stride_blk = p.out_stride_blk;
+  const tzc_epilogue e{ep.kind, ep.scale};
+  auto fail = [](const Status& s) {
+    if (s.code == TZC_E_DEVICE) throw DeviceError(s.msg);
+    throw InjectError(s.msg);
+  };
+  // Problem of `rows` leading units (images for a conv, rows for a GEMM)
+  auto problem = [&](int64_t rows) {
+    Problem pb;
+    Status s;
+    if (p.family == KernelPlan::Family::Matmul) {
+      tzc_gemm_desc g{};
+      g.profile = p.f16 ? TZC_PROFILE_F16 : TZC_PROFILE_U8I8;
+      g.m = (int32_t)rows;
+      g.n = (int32_t)p.k;
+      g.k = (int32_t)p.c;
+      g.b_kn = p.b_kn ? 1 : 0;
+      g.out = ol;
+      s = problem_from_gemm(g, &pb);
+    } else {
+      tzc_conv_desc c{};
+      c.profile = p.f16 ? TZC_PROFILE_F16 : TZC_PROFILE_U8I8;
+      c.n = (int32_t)rows;
+      c.hp = (int32_t)p.hp;
+      c.wp = (int32_t)p.wp;
+      c.c = (int32_t)p.c;
+      c.k = (int32_t)p.k;
+      c.r = (int32_t)p.r;
+      c.s = (int32_t)p.s;
+      c.stride = (int32_t)p.stride;
+      c.w_stride_k = p.w_stride_k;
+      c.w_stride_tap = p.w_stride_tap;
+      c.out = ol;
+      s = problem_from_conv(c, &pb);
+    }
+    if (!s.ok()) throw InjectError(s.msg);
+    return pb;
+  };
+
+  // Batched NHWC conv / row-major GEMM with a dense output: the leading unit
+  // (image / row block) is outermost in data, accumulator image and output,
+  // so the op splits into independent chunks.  Chunk i's H2D, kernel and D2H
+  // go on stream i % 3: the H2D of chunk i+1 and the D2H of chunk i-1 run on
+  // the two copy engines while chunk i computes, and the op costs about
+  // max(H2D, D2H) instead of H2D + kernel + D2H.
+  const bool conv = p.family == KernelPlan::Family::ConvNHWC;
+  const int64_t units = p.family == KernelPlan::Family::Matmul ? p.m : (conv ? p.n : 1);
+  const bool dense_out = ol.nb == (int32_t)p.k && ol.stride_m == p.k;
+  const int64_t per_unit_x = p.family == KernelPlan::Family::Matmul ? p.c : p.hp * p.wp * p.c;
+  const int64_t oh = (p.hp - p.r) / p.stride + 1, ow = (p.wp - p.s) / p.stride + 1;
+  const int64_t per_unit_o = p.family == KernelPlan::Family::Matmul ? p.k : oh * ow * p.k;
+  int64_t chunk = units;
+  if ((conv || p.family == KernelPlan::Family::Matmul) && dense_out && units >= 2) {
+    const int64_t target = p.family == KernelPlan::Family::Matmul ? 8 : std::min<int64_t>(8, units);
+    chunk = (units + target - 1) / target;
+    if (p.family == KernelPlan::Family::Matmul) chunk = std::max<int64_t>(128, (chunk + 127) / 128 * 128);
+  }
+  if (chunk < units) {
+    static cudaStream_t S[3] = {nullptr, nullptr, nullptr};
+    static cudaEvent_t ev_w = nullptr;
+    if (!S[0]) {
+      for (auto& x : S) cuda_ok(cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking), "stream");
+      cuda_ok(cudaEventCreateWithFlags(&ev_w, cudaEventDisableTiming), "event");
+    }
+    const int eb_x = elem_bytes(td.dtype), eb_s = elem_bytes(to.dtype), eb_o = elem_bytes(ep.out_dtype);
+    cuda_ok(cudaMemcpyAsync(dw, hw, wb, cudaMemcpyHostToDevice, S[0]), "H2D weight");
+    cuda_ok(cudaEventRecord(ev_w, S[0]), "event");
+    int i = 0;
+    for (int64_t u0 = 0; u0 < units; u0 += chunk, ++i) {
+      const int64_t nu = std::min(chunk, units - u0);
+      cudaStream_t st = S[i % 3];
+      cuda_ok(cudaStreamWaitEvent(st, ev_w, 0), "wait weights");
+      uint8_t* cx = static_cast<uint8_t*>(dx) + u0 * per_unit_x * eb_x;
+      cuda_ok(cudaMemcpyAsync(cx, static_cast<const uint8_t*>(hx) + u0 * per_unit_x * eb_x, nu * per_unit_x * eb_x,
+                              cudaMemcpyHostToDevice, st),
+              "H2D data");
+      uint8_t* cs = nullptr;
+      if (hs) {
+        cs = static_cast<uint8_t*>(ds) + u0 * per_unit_o * eb_s;
+        cuda_ok(cudaMemcpyAsync(cs, static_cast<const uint8_t*>(hs) + u0 * per_unit_o * eb_s, nu * per_unit_o * eb_s,
+                                cudaMemcpyHostToDevice, st),
+                "H2D accumulator image");
+      }
+      uint8_t* co = static_cast<uint8_t*>(dout) + u0 * per_unit_o * eb_o;
+      const Status s = run_problem(problem(nu), cx, dw, cs, co, e, st);
+      if (!s.ok()) fail(s);
+      cuda_ok(cudaMemcpyAsync(static_cast<uint8_t*>(host_out) + u0 * per_unit_o * eb_o, co, nu * per_unit_o * eb_o,
+                              cudaMemcpyDeviceToHost, st),
+              "D2H output");
+    }
+    for (auto& x : S) cuda_ok(cudaStreamSynchronize(x), "tensorized op");
+    return;
+  }
+
+  cudaStream_t st = nullptr;
   cuda_ok(cudaMemcpyAsync(dx, hx, xb, cudaMemcpyHostToDevice, st), "H2D data");
   cuda_ok(cudaMemcpyAsync(dw, hw, wb, cudaMemcpyHostToDevice, st), "H2D weight");
   if (hs) cuda_ok(cudaMemcpyAsync(ds, hs, sb, cudaMemcpyHostToDevice, st), "H2D accumulator image");
-
-  Problem pb;
-  pb.f16 = p.f16 ? 1 : 0;
   const void* a = dx;
   const void* b = dw;
   if (p.family == KernelPlan::Family::ConvBlocked) {
@@ -539,43 +633,8 @@ void run_tensorized_packed(const TensorizedOp& t, const std::map<std::string, co
     a = ux;
     b = uw;
   }
-  tzc_out_layout ol{};
-  ol.nb = (int32_t)p.out_nb;
-  ol.stride_m = p.out_stride_m;
-  ol.stride_blk = p.out_stride_blk;
-  Status s;
-  if (p.family == KernelPlan::Family::Matmul) {
-    tzc_gemm_desc g{};
-    g.profile = p.f16 ? TZC_PROFILE_F16 : TZC_PROFILE_U8I8;
-    g.m = (int32_t)p.m;
-    g.n = (int32_t)p.k;
-    g.k = (int32_t)p.c;
-    g.b_kn = p.b_kn ? 1 : 0;
-    g.out = ol;
-    s = problem_from_gemm(g, &pb);
-  } else {
-    tzc_conv_desc c{};
-    c.profile = p.f16 ? TZC_PROFILE_F16 : TZC_PROFILE_U8I8;
-    c.n = (int32_t)p.n;
-    c.hp = (int32_t)p.hp;
-    c.wp = (int32_t)p.wp;
-    c.c = (int32_t)p.c;
-    c.k = (int32_t)p.k;
-    c.r = (int32_t)p.r;
-    c.s = (int32_t)p.s;
-    c.stride = (int32_t)p.stride;
-    c.w_stride_k = p.w_stride_k;
-    c.w_stride_tap = p.w_stride_tap;
-    c.out = ol;
-    s = problem_from_conv(c, &pb);
-  }
-  if (!s.ok()) throw InjectError(s.msg);
-  tzc_epilogue e{ep.kind, ep.scale};
-  s = run_problem(pb, a, b, ds, dout, e, st);
-  if (!s.ok()) {
-    if (s.code == TZC_E_DEVICE) throw DeviceError(s.msg);
-    throw InjectError(s.msg);
-  }
+  const Status s = run_problem(problem(p.family == KernelPlan::Family::Matmul ? p.m : p.n), a, b, ds, dout, e, st);
+  if (!s.ok()) fail(s);
   cuda_ok(cudaMemcpyAsync(host_out, dout, (size_t)out_bytes, cudaMemcpyDeviceToHost, st), "D2H output");
   cuda_ok(cudaStreamSynchronize(st), "tensorized op");
 }

@@ -332,7 +332,10 @@ __device__ __forceinline__ void store16(const ConvKernelParams& p, int m, int n,
 // when BN >= 128: 4 warps per SMSP hide the tcgen05.ld / STG latency).
 template <int BN>
 struct EpiCfg {
-  static constexpr int WARPS = 16;
+#ifndef TZC_EPI_WARPS64
+#define TZC_EPI_WARPS64 16
+#endif
+  static constexpr int WARPS = BN == 64 ? TZC_EPI_WARPS64 : 16;
   static constexpr int GROUPS = WARPS / 4;     // column groups per lane quarter
   static constexpr int COLS = BN / GROUPS;     // columns per epilogue warp (16, 32 or 64)
   static constexpr int CW = COLS < 32 ? COLS : 32;  // columns per tcgen05.ld chunk
@@ -599,7 +602,7 @@ __global__ void __launch_bounds__(EpiCfg<BN>::THREADS, 1) conv_tc_kernel(const _
         constexpr int RB = BN < 128 ? BN : 128;
         uint8_t* stq = sStage + q * (32 * BN);
         if (h == 0 && lane == 0) bulk_wait_read0();  // previous tile's store has read the staging
-        named_bar_sync(1 + q, 128);
+        named_bar_sync(1 + q, 32 * EpiCfg<BN>::GROUPS);
 #pragma unroll 1
         for (int c = 0; c < HALF / CW; ++c) {
           const int col = h * HALF + c * CW;
@@ -608,7 +611,7 @@ __global__ void __launch_bounds__(EpiCfg<BN>::THREADS, 1) conv_tc_kernel(const _
                                         smem_u32(stq), (int)lane, col);
         }
         fence_proxy_async_smem();
-        named_bar_sync(1 + q, 128);
+        named_bar_sync(1 + q, 32 * EpiCfg<BN>::GROUPS);
         if (h == 0 && lane == 0) {
 #pragma unroll
           for (int b = 0; b < BN / RB; ++b) tma_store_2d(&p.tmO, stq + b * (32 * RB), n_tile * BN + b * RB, m_tile * BM + q * 32);

@@ -59,12 +59,24 @@ def test_run_op_matmul_requant_and_no_seed(cuda):
     assert np.array_equal(ops.run_op(text, "tcgen05_i8_m128n256k32", no_seed), Orc.matmul(ins["A"], ins["B"]))
 
 
-@pytest.mark.parametrize("n,h,c,k,r,st", [(2, 12, 64, 128, 3, 1), (2, 21, 3, 64, 7, 2), (1, 14, 256, 512, 1, 2)])
+@pytest.mark.parametrize("n,h,c,k,r,st", [(2, 12, 64, 128, 3, 1), (2, 21, 3, 64, 7, 2), (1, 14, 256, 512, 1, 2),
+                                           (11, 10, 64, 64, 3, 1), (9, 29, 3, 64, 7, 2)])
 def test_run_op_conv_nhwc(cuda, n, h, c, k, r, st):
+    """Batched ops run as image chunks over three streams (H2D / kernel / D2H
+    overlapped): uneven chunk counts, seeds and the fused requant stay exact."""
     text = conv2d_nhwc_tdsl(n, h, h, c, k, r, r, st)
     ins = Orc.random_inputs(decls(text), 5)
     ref = Orc.conv2d_nhwc(ins["data"], ins["kernel"], st, ins["out"])
     assert np.array_equal(ops.run_op(text, "tcgen05_i8_m128n64k32", ins), ref)
+    q = ops.run_op(text, "tcgen05_i8_m128n64k32", ins, epilogue=requant_tdsl(ref.shape, 2.0 ** -11, src="out"))
+    assert np.array_equal(q, Orc.requant_i8(ref, 2.0 ** -11))
+
+
+def test_run_op_matmul_chunked_uneven(cuda):
+    text = matmul_tdsl(1000, 128, 96)
+    ins = Orc.random_inputs(decls(text), 78)
+    ref = Orc.matmul(ins["A"], ins["B"], ins["C"])
+    assert np.array_equal(ops.run_op(text, "tcgen05_i8_m128n128k32", ins), ref)
 
 
 def test_run_op_errors(cuda):
