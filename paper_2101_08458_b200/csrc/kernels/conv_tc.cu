@@ -271,6 +271,8 @@ Problem k7_gemm(const Problem& pb, int* kp_out) {
 
 struct WsPlan {
   int bn = 0, kb = 0, pair = 0, c_blocks = 0, sr = 0, box_rows = 0, a_slots = 0, smem = 0, tiles = 0, grid = 0;
+  int mt = 1;  // 128-row tiles per work unit
+  int halo = 0;
   int64_t p_rows = 0;
 };
 bool ws_plan(const Problem& pb, bool pair, WsPlan* w);
@@ -285,7 +287,7 @@ Status plan_problem(const Problem& pb_in, tzc_plan* plan) {
     const Problem q = s2d ? s2d_problem(pb_in) : pb_in;
     WsPlan w;
     if ((s2d || (!needs_k7(pb_in) && g_ws_enabled)) && ws_plan(q, s2d, &w)) {
-      plan->bm = 128;
+      plan->bm = 128 * w.mt;  // rows per work unit
       plan->bn = w.bn;
       plan->bk_bytes = w.kb;
       plan->stages = w.a_slots;
@@ -366,10 +368,12 @@ void ws_boxes(const WsPlan& w, int* nbox, int* box_rows, int* box_bytes, int* di
     *box_bytes = *box_rows * 128;
     return;
   }
+  // <= 256-row boxes, each a multiple of 8 rows so consecutive boxes continue
+  // the swizzle pattern of one contiguous super-tile
   *div = 1;
-  *box_rows = w.box_rows;
-  *nbox = w.sr > w.box_rows ? 2 : 1;
-  *box_bytes = w.box_rows * w.kb;
+  *nbox = (w.sr + 255) / 256;
+  *box_rows = ((w.sr + *nbox - 1) / *nbox + 7) / 8 * 8;
+  *box_bytes = *box_rows * w.kb;
 }
 
 int ws_smem(const WsPlan& w, int taps) {
@@ -436,7 +440,8 @@ bool ws_plan(const Problem& pb, bool pair, WsPlan* w) {
   x.bn = pb.ngemm;
   x.pair = pair ? 1 : 0;
   if (pair) {
-    if (cb != 16 || pb.s % 2 || pb.f16) return false;
+    // the pair kernel is specialised for the 4 x 4-tap space-to-depth stem (8 MMAs per tile)
+    if (cb != 16 || pb.r != 4 || pb.s != 4 || pb.f16) return false;
     x.kb = 16;
   } else {
     x.kb = cb % 128 == 0 ? 128 : (cb % 64 == 0 ? 64 : 0);
@@ -445,21 +450,39 @@ bool ws_plan(const Problem& pb, bool pair, WsPlan* w) {
   x.c_blocks = (int)(cb / x.kb);
   if ((pair ? pb.taps / 2 : pb.taps * (x.kb / 32)) > 64) return false;  // ConvKernelParams::mma_a capacity
   if ((int64_t)pb.taps * x.c_blocks * x.bn * x.kb > 160 * 1024) return false;  // weights must stay resident
-  x.sr = 128 + (pb.r - 1) * pb.wp + (pb.s - 1);
-  if (x.sr > 512) return false;
-  x.box_rows = x.sr <= 256 ? x.sr : (((x.sr + 1) / 2 + 7) / 8) * 8;
+  x.halo = (pb.r - 1) * pb.wp + (pb.s - 1);
+  if (128 + x.halo > 1024) return false;
   // padded-grid waste: (Hp*Wp)/(OH*OW) extra MMA rows
   if ((double)pb.hp * pb.wp > 1.35 * (double)pb.oh * pb.ow) return false;
   x.p_rows = (int64_t)pb.n * pb.hp * pb.wp;
   if (x.p_rows + 128 >= (int64_t(1) << 22) || (int64_t)pb.hp * pb.wp >= (1 << 18)) return false;  // exact magic division
-  for (x.a_slots = 6; x.a_slots >= 2; --x.a_slots)
-    if (ws_smem(x, pb.taps) <= 227 * 1024 - kStaticSmem) break;
-  if (x.a_slots < 2) return false;
-  x.smem = ws_smem(x, pb.taps);
-  x.tiles = (int)((x.p_rows + 127) / 128);
-  x.grid = std::min(x.tiles, num_sms());
-  *w = x;
-  return true;
+  const int tiles = (int)((x.p_rows + 127) / 128);
+  const int sms = num_sms();
+  // MT tiles per unit: the largest that fits TMEM (2*MT*BN <= 512) and SMEM
+  // (>= 2 super-tile slots next to the resident weights), keeps every CTA
+  // busy for >= 8 units and loses <= 6% to the last round's imbalance
+  for (int mt : {4, 2, 1}) {
+    if (2 * mt * x.bn > 512) continue;
+    const int units = (tiles + mt - 1) / mt;
+    if (mt > 1) {
+      if (units < 8 * sms) continue;
+      const double rounds = std::ceil((double)units / sms), ideal = (double)units / sms;
+      if (rounds > 1.06 * ideal) continue;
+    }
+    WsPlan y = x;
+    y.mt = mt;
+    y.sr = mt * 128 + x.halo;
+    for (y.a_slots = 6; y.a_slots >= 2; --y.a_slots)
+      if (ws_smem(y, pb.taps) <= 227 * 1024 - kStaticSmem) break;
+    if (y.a_slots < 2) continue;
+    if (mt > 1 && y.a_slots < 3) continue;  // a deeper ring beats a bigger unit
+    y.smem = ws_smem(y, pb.taps);
+    y.tiles = units;
+    y.grid = std::min(units, sms);
+    *w = y;
+    return true;
+  }
+  return false;
 }
 
 Status run_ws(const Problem& pb, const WsPlan& w, const void* a, const void* b, const void* seed, void* out,
@@ -540,6 +563,7 @@ Status run_ws(const Problem& pb, const WsPlan& w, const void* a, const void* b, 
   p.a_coord_div = div;
   p.num_tiles = w.tiles;
   p.splits = w.a_slots;  // ring depth (the kernel has no split-K)
+  p.mt = w.mt;
   fill_epilogue(&p, pb, seed, out, ep);
   WsFn fn = ws_fn(w.bn, w.kb, pb.f16 != 0, w.pair != 0);
   if (!fn) return Status(TZC_E_INTERNAL, "no conv_ws instantiation");
@@ -758,6 +782,10 @@ Status run_problem(const Problem& pb, const void* a, const void* b, const void* 
 
 #ifdef TZC_TRACE
 extern "C" void tzc_debug_flags(int f) { g_debug_flags = f; }
+extern "C" void tzc_trace_cta(unsigned long long* out /* [2][1024] */) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out, tzcdev::g_cta_t, sizeof(unsigned long long) * 2048);
+}
 extern "C" void tzc_trace_dump(unsigned long long* out) {
   cudaDeviceSynchronize();
   cudaMemcpyFromSymbol(out, tzcdev::g_trace, sizeof(unsigned long long) * 128);

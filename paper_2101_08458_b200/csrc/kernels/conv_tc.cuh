@@ -33,6 +33,12 @@
 #ifdef TZC_TRACE
 namespace tzcdev {
 __device__ unsigned long long g_trace[128];
+__device__ unsigned long long g_cta_t[2][1024];  // per-CTA %globaltimer at start / end (ns)
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 }
 // recorded in shared memory (no global stores perturbing the timeline),
 // copied out by thread 0 of CTA 0 at kernel end
@@ -40,6 +46,7 @@ __device__ unsigned long long g_trace[128];
 #define TZC_TRACE_INIT                                  \
   do {                                                  \
     if (threadIdx.x < 128) s_trace[threadIdx.x] = 0ull; \
+    if (threadIdx.x == 0 && blockIdx.x < 1024) tzcdev::g_cta_t[0][blockIdx.x] = tzcdev::gtimer(); \
   } while (0)
 #define TZC_TRACE_POINT(i)                                 \
   do {                                                     \
@@ -52,6 +59,7 @@ __device__ unsigned long long g_trace[128];
 #define TZC_TRACE_FLUSH                                                         \
   do {                                                                          \
     if (blockIdx.x == 0 && threadIdx.x < 128) tzcdev::g_trace[threadIdx.x] = s_trace[threadIdx.x]; \
+    if (threadIdx.x == 0 && blockIdx.x < 1024) tzcdev::g_cta_t[1][blockIdx.x] = tzcdev::gtimer(); \
   } while (0)
 #else
 #define TZC_TRACE_DECL
@@ -116,6 +124,7 @@ struct alignas(64) ConvKernelParams {
   int32_t a_nbox, a_box_bytes, a_coord_div;  // A boxes per super-tile, bytes per box, pixel rows per TMA row
   int32_t simple;              // requant, 2^-k (k>=2), no seed, no range check, row-major, aligned
   int32_t tma_store;           // int8 tile staged in SMEM, written by TMA (full-line stores)
+  int32_t mt;                  // shifted-window: 128-row tiles per work unit
   uint64_t magic_hw, magic_wp; // ceil(2^40 / (Hp*Wp)), ceil(2^40 / Wp): exact q / d for q < 2^22
   int32_t debug_flags;         // tools only: 1 = skip epilogue body, 2 = skip epilogue stores
   // shifted-window MMA table: per MMA of a channel block, the A start-address
@@ -376,16 +385,11 @@ __device__ __forceinline__ void epi_simple(const ConvKernelParams& p, int m, int
 }
 
 // One tcgen05.ld chunk of CW accumulator columns for row m (m < 0: no row).
+// CW accumulator columns already in registers, row m (m < 0: no row), column n.
 // stg != 0: int8 results go to the TMA staging tile (row srow, column scol of the tile)
 template <int CW, bool kF16, int kEpm, int BN>
-__device__ __forceinline__ void epi_chunk(const ConvKernelParams& p, uint32_t taddr, int m, int n, bool fast,
-                                          uint32_t stg = 0, int srow = 0, int scol = 0) {
-  uint32_t v[CW];
-  if constexpr (CW == 16)
-    tmem_ld16(taddr, v);
-  else
-    tmem_ld32(taddr, v);
-  tmem_ld_wait();
+__device__ __forceinline__ void epi_regs(const ConvKernelParams& p, const uint32_t* v, int m, int n, bool fast,
+                                         uint32_t stg = 0, int srow = 0, int scol = 0) {
   if (m < 0) return;
   if constexpr (kEpm == EPM_REQUANT) {
     if (p.simple) {
@@ -402,6 +406,24 @@ __device__ __forceinline__ void epi_chunk(const ConvKernelParams& p, uint32_t ta
     for (int j = 0; j < CW / 16; ++j)
       if (n + 16 * j < p.Ngemm) store16<kF16, kEpm, false>(p, m, n + 16 * j, v + 16 * j);
   }
+}
+
+template <int CW>
+__device__ __forceinline__ void tmem_ld_cw(uint32_t taddr, uint32_t* v) {
+  if constexpr (CW == 16)
+    tmem_ld16(taddr, *reinterpret_cast<uint32_t(*)[16]>(v));
+  else
+    tmem_ld32(taddr, *reinterpret_cast<uint32_t(*)[32]>(v));
+}
+
+// One tcgen05.ld chunk of CW accumulator columns for row m (m < 0: no row).
+template <int CW, bool kF16, int kEpm, int BN>
+__device__ __forceinline__ void epi_chunk(const ConvKernelParams& p, uint32_t taddr, int m, int n, bool fast,
+                                          uint32_t stg = 0, int srow = 0, int scol = 0) {
+  uint32_t v[CW];
+  tmem_ld_cw<CW>(taddr, v);
+  tmem_ld_wait();
+  epi_regs<CW, kF16, kEpm, BN>(p, v, m, n, fast, stg, srow, scol);
 }
 
 template <int BN, int KB, bool kF16, int kAMode, bool kBMN, int kEpm>

@@ -20,6 +20,11 @@
 // 12(+4) channels).  SWIZZLE_NONE rows at 16-byte pitch; one K=32 MMA covers
 // taps (r, s) and (r, s+1) by setting the descriptor's leading-byte offset
 // to 16 B — the next row — (hardware-verified, tools/desc_probe.cu).
+//
+// Work unit = MT consecutive 128-row tiles (host-chosen, p.mt; 2*MT*BN TMEM
+// columns): one A super-tile of MT*128 + halo rows feeds MT accumulators, so
+// the halo re-read ((R-1)*Wp+(S-1) rows) and the per-unit barrier / commit /
+// epilogue hand-off costs are paid once per MT tiles.
 #pragma once
 #include "conv_tc.cuh"
 
@@ -41,7 +46,7 @@ __global__ void __launch_bounds__(EpiCfg<BN>::THREADS, 1) conv_ws_kernel(const _
   constexpr int BM = 128;
   constexpr int KE = kF16 ? KB / 2 : KB;
   constexpr uint32_t IDESC = kF16 ? idesc_f16(BM, BN, false) : idesc_i8(BM, BN);
-  constexpr uint32_t TMEM_COLS = ConvCfg<BN, KB>::TMEM_COLS;
+  constexpr uint32_t TMEM_COLS = 512;  // 2 accumulators x MT tiles x BN (MT <= 256 / BN)
   const int taps = p.R * p.S;
   const int c_blocks = p.c_blocks;
   const int b_tile = BN * KB;                                     // one (tap, channel block) of weights
@@ -88,7 +93,8 @@ __global__ void __launch_bounds__(EpiCfg<BN>::THREADS, 1) conv_ws_kernel(const _
   pdl_launch_dependents();
   pdl_wait();
 
-  const int num_tiles = p.num_tiles;
+  const int num_tiles = p.num_tiles;  // work units of MT tiles
+  const int MT = p.mt;
   if (warp == 0) {
     if (lane == 0) {
       // stationary weights: every (tap, channel block) tile, once
@@ -103,16 +109,16 @@ __global__ void __launch_bounds__(EpiCfg<BN>::THREADS, 1) conv_ws_kernel(const _
       int slot = 0;
       uint32_t phase = 0;
       for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-        const int q0 = tile * BM;
+        const int q0 = tile * MT * BM;
         const int it = (tile - (int)blockIdx.x) / (int)gridDim.x;
         for (int cb = 0; cb < c_blocks; ++cb) {
           mbar_wait(&aempty[slot], phase ^ 1);
           if (it < 10) TZC_TRACE_POINT(10 + 5 * it);
           uint8_t* dA = sA + slot * a_slot;
           mbar_expect_tx(&afull[slot], p.a_nbox * p.a_box_bytes);
-          const int row0 = q0 / p.a_coord_div;  // pair mode: 8 pixels per 128-byte TMA row
-          tma_load_2d(dA, &p.tmA, &afull[slot], cb * KE, row0);
-          if (p.a_nbox > 1) tma_load_2d(dA + p.a_box_bytes, &p.tmA, &afull[slot], cb * KE, row0 + p.box_rows);
+          const int row0 = kPair ? q0 >> 3 : q0;  // pair mode: 8 pixels per 128-byte TMA row
+          for (int b = 0; b < p.a_nbox; ++b)
+            tma_load_2d(dA + b * p.a_box_bytes, &p.tmA, &afull[slot], cb * KE, row0 + b * p.box_rows);
           if (++slot == a_slots) {
             slot = 0;
             phase ^= 1;
@@ -127,6 +133,15 @@ __global__ void __launch_bounds__(EpiCfg<BN>::THREADS, 1) conv_ws_kernel(const _
     // and issues UTCIMMA back to back; a lane-0 loop pays ~125 cycles per MMA
     // in R2UR + elect waterfalls, above the 48-cycle N=64 MMA (tools/mma_rate.cu).
     const uint32_t b_base = smem_u32(sB);
+    constexpr int MT_PAIR_MAX = 4;
+    uint32_t pa[8], pb[8];
+    if constexpr (kPair) {  // host guarantees n_mma == 8 (4 x 4 taps) in pair mode
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        pa[i] = p.mma_a[i];
+        pb[i] = p.mma_b[i];
+      }
+    }
     mbar_wait(bfull, 0);
     int slot = 0;
     uint32_t phase = 0;
@@ -135,7 +150,7 @@ __global__ void __launch_bounds__(EpiCfg<BN>::THREADS, 1) conv_ws_kernel(const _
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
       mbar_wait(&tempty[acc], acc_phase ^ 1);
       tc_fence_after();
-      const uint32_t tmem_d = tmem_base + acc * BN;
+      const uint32_t tmem_acc = tmem_base + acc * (MT * BN);
       const int it = (tile - (int)blockIdx.x) / (int)gridDim.x;
       if (lane == 0 && it < 10) TZC_TRACE_POINT(11 + 5 * it);
       for (int cb = 0; cb < c_blocks; ++cb) {
@@ -148,17 +163,30 @@ __global__ void __launch_bounds__(EpiCfg<BN>::THREADS, 1) conv_ws_kernel(const _
           const uint32_t b_cb = b_base + (kPair ? 0u : (uint32_t)(cb * b_tile));
           const uint64_t b0 = kPair ? smem_desc_none(b_cb, BN * 16, 128) : smem_desc_kmajor(b_cb, KB);
           const int n_mma = p.n_mma;
-#ifdef TZC_TRACE
-          if (p.debug_flags & 12) {
-            for (int i = 0; i < n_mma; ++i)
-              if (elect_one())
-                umma<kF16>(tmem_d, a0 + ((p.debug_flags & 4) ? 0 : p.mma_a[i]), b0 + ((p.debug_flags & 8) ? 0 : p.mma_b[i]),
-                           IDESC, (cb > 0 || i > 0) ? 1u : 0u);
-          } else
-#endif
+          if constexpr (kPair) {
+            // the space-to-depth stem: 4 x 4 taps, two per MMA = 8 MMAs per
+            // tile, offsets held in uniform registers for the whole kernel
+            // (a constant-bank load per MMA put its latency on the issue path)
+#pragma unroll
+            for (int t = 0; t < MT_PAIR_MAX; ++t) {
+              if (t < MT) {
+                const uint64_t at = a0 + (uint64_t)(t * 128);
+                const uint32_t tmem_d = tmem_acc + t * BN;
+#pragma unroll
+                for (int i = 0; i < 8; ++i)
+                  if (elect_one()) umma<kF16>(tmem_d, at + pa[i], b0 + pb[i], IDESC, i > 0 ? 1u : 0u);
+              }
+            }
+          } else {
+            for (int t = 0; t < MT; ++t) {
+              // tile t of the unit: A rows shifted by t*128 (16-byte descriptor units)
+              const uint64_t at = a0 + (uint64_t)(t * 8 * KB);
+              const uint32_t tmem_d = tmem_acc + t * BN;
 #pragma unroll 2
-          for (int i = 0; i < n_mma; ++i)
-            if (elect_one()) umma<kF16>(tmem_d, a0 + p.mma_a[i], b0 + p.mma_b[i], IDESC, (cb > 0 || i > 0) ? 1u : 0u);
+              for (int i = 0; i < n_mma; ++i)
+                if (elect_one()) umma<kF16>(tmem_d, at + p.mma_a[i], b0 + p.mma_b[i], IDESC, (cb > 0 || i > 0) ? 1u : 0u);
+            }
+          }
           if (elect_one()) {
             umma_commit(&aempty[slot]);
             if (cb == c_blocks - 1) umma_commit(&tfull[acc]);
@@ -184,30 +212,33 @@ __global__ void __launch_bounds__(EpiCfg<BN>::THREADS, 1) conv_ws_kernel(const _
     const int hw = p.Hp * p.Wp;
     int acc = 0;
     uint32_t acc_phase = 0;
+    constexpr int CW = EpiCfg<BN>::CW;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-      const int q = tile * BM + q4 * 32 + lane;
-      int m = -1;
-      if (q < p.P) {  // exact magic-number division (q < 2^22 host-checked)
-        const int n = (int)(((uint64_t)q * p.magic_hw) >> 40), rem = q - n * hw;
-        const int oh = (int)(((uint64_t)rem * p.magic_wp) >> 40), ow = rem - oh * p.Wp;
-        if (oh < p.OH && ow < p.OWv) m = (n * p.OH + oh) * p.OWv + ow;
-      }
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const int it = (tile - (int)blockIdx.x) / (int)gridDim.x;
       if (threadIdx.x == 128 && it < 10) TZC_TRACE_POINT(13 + 5 * it);
-      if (!(p.debug_flags & 1)) {
-        constexpr int CW = EpiCfg<BN>::CW;
-        const bool fast = p.vec_ok && BN <= p.Ngemm;
+      for (int t = 0; t < MT; ++t) {
+        const int q = (tile * MT + t) * BM + q4 * 32 + lane;
+        int m = -1;
+        if (q < p.P) {  // exact magic-number division (q < 2^22 host-checked)
+          const int n = (int)(((uint64_t)q * p.magic_hw) >> 40), rem = q - n * hw;
+          const int oh = (int)(((uint64_t)rem * p.magic_wp) >> 40), ow = rem - oh * p.Wp;
+          if (oh < p.OH && ow < p.OWv) m = (n * p.OH + oh) * p.OWv + ow;
+        }
+        if (!(p.debug_flags & 1)) {
+          const bool fast = p.vec_ok && BN <= p.Ngemm;
 #pragma unroll 1
-        for (int c = 0; c < COLS / CW; ++c)
-          epi_chunk<CW, kF16, kEpm, BN>(p, tmem_base + ((q4 * 32) << 16) + acc * BN + h * COLS + c * CW,
-                                    (p.debug_flags & 2) ? -1 : m, h * COLS + c * CW, fast);
+          for (int c = 0; c < COLS / CW; ++c)
+            epi_chunk<CW, kF16, kEpm, BN>(
+                p, tmem_base + ((q4 * 32) << 16) + acc * (MT * BN) + t * BN + h * COLS + c * CW,
+                (p.debug_flags & 2) ? -1 : m, h * COLS + c * CW, fast);
+        }
       }
       tc_fence_before();
       __syncwarp();
-      if (threadIdx.x == 128 && it < 10) TZC_TRACE_POINT(14 + 5 * it);
       if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (threadIdx.x == 128 && it < 10) TZC_TRACE_POINT(14 + 5 * it);
       if (++acc == 2) {
         acc = 0;
         acc_phase ^= 1;

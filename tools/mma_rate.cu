@@ -95,10 +95,19 @@ __global__ void __launch_bounds__(640, 1) mma_rate(int tiles, int wp, int kb, lo
     if (elect_one()) umma_commit(&fin);
   }
   else if (MODE >= 3 && warp == 0) {
-    const uint64_t a0 = smem_desc_kmajor(smem_u32(sm), kb), b0 = smem_desc_kmajor(smem_u32(sm) + 96 * 1024, kb);
+    // MODE 6: pair-mode (SWIZZLE_NONE, LBO = 16 B: two consecutive 16-byte pixels per K=32) descriptors
+    const uint64_t a0 = MODE == 6 ? (((uint64_t)(smem_u32(sm) >> 4) & 0x3FFF) | (1ull << 16) | (8ull << 32) | (1ull << 46))
+                                  : smem_desc_kmajor(smem_u32(sm), kb);
+    const uint64_t b0 = MODE == 6 ? (((uint64_t)((smem_u32(sm) + 96 * 1024) >> 4) & 0x3FFF) | ((uint64_t)(NB * 16 >> 4) << 16) |
+                                     (8ull << 32) | (1ull << 46))
+                                  : smem_desc_kmajor(smem_u32(sm) + 96 * 1024, kb);
     for (int t = 0; t < tiles; ++t) {
       const uint32_t d = tmem + (t & 1) * NB;
-      if (MODE == 5) {
+      if (MODE == 6) {
+#pragma unroll 2
+        for (int i = 0; i < ct.n; ++i)
+          if (elect_one()) umma<false>(d, a0 + ct.a[i], b0 + ct.b[i], idesc, i > 0);
+      } else if (MODE == 5) {
         for (int i = 0; i < ct.n; ++i)
           if (elect_one()) umma<false>(d, a0, b0, idesc, i > 0);
       } else if (MODE == 3) {
@@ -204,6 +213,25 @@ int main() {
     printf("try_wait(done) %.1f  +fence %.1f  test_wait spin %.1f  commit %.1f cyc\n", c[0] / 1000.0, c[1] / 1000.0,
            c[2] / 1000.0, c[3] / 1000.0);
   }
+  auto run_pair = [&](auto kern, const char* name, int wp, int salign) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    Tab ct{};
+    ct.n = 8;
+    for (int r = 0, i = 0; r < 4; ++r)
+      for (int s2 = 0; s2 < 4; s2 += 2, ++i) {
+        ct.a[i] = (uint32_t)(r * wp + s2 * salign);  // 16-byte pixels
+        ct.b[i] = (uint32_t)(((r * 4 + s2) * 64 * 16) >> 4);
+      }
+    kern<<<148, 640, 200 * 1024>>>(tiles, wp, 16, dc, ct);
+    cudaDeviceSynchronize();
+    long long c;
+    cudaMemcpy(&c, dc, 8, cudaMemcpyDeviceToHost);
+    printf("%-22s wp %3d salign %d: %.1f cyc/MMA\n", name, wp, salign, c / (double)(tiles * 8));
+  };
+  run_pair(mma_rate<64, 6>, "pair N=64", 115, 1);
+  run_pair(mma_rate<64, 6>, "pair N=64", 120, 1);
+  run_pair(mma_rate<64, 6>, "pair N=64", 120, 4);
+  run_pair(mma_rate<64, 6>, "pair N=64", 0, 0);
   for (int kb : {64}) {
     run(mma_rate<64, 0>, "N=64 lane0+table", kb);
     run(mma_rate<64, 1>, "N=64 uniform", kb);

@@ -5,11 +5,14 @@
 
 #include <cstdio>
 #include <cstdlib>
+#include <algorithm>
+#include <vector>
 
 #include "tzc_b200.h"
 
 extern "C" void tzc_trace_dump(unsigned long long* out);
 extern "C" void tzc_debug_flags(int f);
+extern "C" void tzc_trace_cta(unsigned long long* out);
 
 int main(int argc, char** argv) {
   int n = argc > 1 ? atoi(argv[1]) : 256, hp = argc > 2 ? atoi(argv[2]) : 230, c = argc > 3 ? atoi(argv[3]) : 3;
@@ -42,6 +45,28 @@ int main(int argc, char** argv) {
     unsigned long long t[128];
     tzc_trace_dump(t);
     printf("iter %d: %.1f us total\n", it, ms * 1000);
+    {
+      static unsigned long long ct[2][1024];
+      tzc_trace_cta(&ct[0][0]);
+      unsigned long long s0 = ~0ull, s1 = 0, e0 = ~0ull, e1 = 0;
+      int nc = 0;
+      for (int b = 0; b < 1024; ++b) {
+        if (!ct[0][b] || ct[1][b] < ct[0][b]) continue;
+        ++nc;
+        s0 = std::min(s0, ct[0][b]); s1 = std::max(s1, ct[0][b]);
+        e0 = std::min(e0, ct[1][b]); e1 = std::max(e1, ct[1][b]);
+      }
+      printf("  CTAs %d: start spread %.2f us, end min %.2f max %.2f us after first start\n", nc, (s1 - s0) / 1e3,
+             (e0 - s0) / 1e3, (e1 - s0) / 1e3);
+      std::vector<double> ends;
+      for (int b = 0; b < 1024; ++b)
+        if (ct[0][b] && ct[1][b] >= ct[0][b]) ends.push_back((ct[1][b] - s0) / 1e3);
+      std::sort(ends.begin(), ends.end());
+      if (!ends.empty())
+        printf("  end percentiles: p10 %.2f p50 %.2f p90 %.2f us\n", ends[ends.size() / 10], ends[ends.size() / 2],
+               ends[ends.size() * 9 / 10]);
+      cudaMemset(nullptr, 0, 0);
+    }
     for (int i = 0; i < 10; ++i)
       printf("  tile %d: prodA=%lld mmaStart=%lld aReady=%lld issued=%lld epiStart=%lld epiEnd=%lld\n", i, (long long)(t[10 + 5 * i] - t[0]),
              (long long)(t[11 + 5 * i] - t[0]), (long long)(t[12 + 5 * i] - t[0]), (long long)(t[70 + i] - t[0]), (long long)(t[13 + 5 * i] - t[0]),
