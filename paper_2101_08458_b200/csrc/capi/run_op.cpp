@@ -34,15 +34,16 @@ struct Cached {
 std::mutex g_mu;
 std::map<std::pair<std::string, std::string>, Cached> g_cache;
 
-const tzc::TensorizedOp& tensorized(const std::string& op_text, const std::string& intr_ref) {
+// std::map nodes are stable: the pointer stays valid for the process lifetime
+const tzc::TensorizedOp* tensorized(const std::string& op_text, const std::string& intr_ref) {
   std::lock_guard<std::mutex> lk(g_mu);
   auto key = std::make_pair(op_text, intr_ref);
   auto it = g_cache.find(key);
-  if (it != g_cache.end()) return it->second.t;
+  if (it != g_cache.end()) return &it->second.t;
   tzc::ComputeOp op = tzc::infer_types(tzc::parse_compute(op_text));
   tzc::Intrinsic intr = tzc::resolve_intrinsic(intr_ref);
   Cached c{tzc::tensorize(op, intr)};
-  return g_cache.emplace(key, std::move(c)).first->second.t;
+  return &g_cache.emplace(key, std::move(c)).first->second.t;
 }
 
 }  // namespace
@@ -53,7 +54,7 @@ extern "C" TZC_API int tzc_b200_run_op(const char* op_tdsl, const char* intrinsi
   try {
     if (!op_tdsl || !intrinsic || !host_out || (n_inputs > 0 && (!names || !host_inputs)))
       throw tzc::MissingInput("NULL argument");
-    const tzc::TensorizedOp& t = tensorized(op_tdsl, intrinsic);
+    const tzc::TensorizedOp& t = *tensorized(op_tdsl, intrinsic);
     std::map<std::string, const void*> in;
     for (int32_t i = 0; i < n_inputs; ++i) in[names[i]] = host_inputs[i];
     if (requant_tdsl) {
@@ -116,7 +117,7 @@ extern "C" TZC_API int tzc_b200_inspect(const char* op_tdsl, const char* intrins
 
 extern "C" TZC_API int tzc_b200_describe(const char* op_tdsl, const char* intrinsic, char* buf, int64_t n) {
   return guarded([&] {
-    const tzc::TensorizedOp& t = tensorized(op_tdsl, intrinsic);
+    const tzc::TensorizedOp& t = *tensorized(op_tdsl, intrinsic);
     std::string s = "mapping " + t.mapping.to_string() + "\nplan " + t.plan.describe() + "\n";
     for (const auto& l : t.schedule) s += l + "\n";
     return put(s, buf, n);

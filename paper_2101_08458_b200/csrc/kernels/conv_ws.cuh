@@ -208,17 +208,20 @@ __global__ void __launch_bounds__(EpiCfg<BN>::THREADS, 1) conv_ws_kernel(const _
     // ===================== epilogue: padded grid -> output rows =====================
     const uint32_t q4 = warp & 3;
     const uint32_t h = (warp - 4) >> 2;
-    constexpr int COLS = EpiCfg<BN>::COLS;
     const int hw = p.Hp * p.Wp;
     int acc = 0;
     uint32_t acc_phase = 0;
-    constexpr int CW = EpiCfg<BN>::CW;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const int it = (tile - (int)blockIdx.x) / (int)gridDim.x;
       if (threadIdx.x == 128 && it < 10) TZC_TRACE_POINT(13 + 5 * it);
-      for (int t = 0; t < MT; ++t) {
+      {
+        // 16 warps over MT tiles: G = 4 / MT column groups per tile, so warp
+        // (q4, h) owns tile h / G, columns (h % G) * BN / G ... — one row-decode
+        // per unit, and with MT = 4 whole output rows per thread (full sectors)
+        const int G = 4 / MT;
+        const int t = (int)h / G, cols = BN / G, col0 = ((int)h % G) * cols;
         const int q = (tile * MT + t) * BM + q4 * 32 + lane;
         int m = -1;
         if (q < p.P) {  // exact magic-number division (q < 2^22 host-checked)
@@ -226,13 +229,16 @@ __global__ void __launch_bounds__(EpiCfg<BN>::THREADS, 1) conv_ws_kernel(const _
           const int oh = (int)(((uint64_t)rem * p.magic_wp) >> 40), ow = rem - oh * p.Wp;
           if (oh < p.OH && ow < p.OWv) m = (n * p.OH + oh) * p.OWv + ow;
         }
+        if (p.debug_flags & 2) m = -1;
+        const uint32_t tq = tmem_base + ((q4 * 32) << 16) + acc * (MT * BN) + t * BN + col0;
         if (!(p.debug_flags & 1)) {
           const bool fast = p.vec_ok && BN <= p.Ngemm;
+          if (cols == 16) {
+            epi_chunk<16, kF16, kEpm, BN>(p, tq, m, col0, fast);
+          } else {
 #pragma unroll 1
-          for (int c = 0; c < COLS / CW; ++c)
-            epi_chunk<CW, kF16, kEpm, BN>(
-                p, tmem_base + ((q4 * 32) << 16) + acc * (MT * BN) + t * BN + h * COLS + c * CW,
-                (p.debug_flags & 2) ? -1 : m, h * COLS + c * CW, fast);
+            for (int c = 0; c < cols / 32; ++c) epi_chunk<32, kF16, kEpm, BN>(p, tq + 32 * c, m, col0 + 32 * c, fast);
+          }
         }
       }
       tc_fence_before();
