@@ -34,6 +34,13 @@ constexpr int kStaticSmem = 1024;  // s_trace
 #else
 constexpr int kStaticSmem = 0;
 #endif
+// General-kernel SMEM: EG int8 staging tiles (128 x BN) + the A/B ring + barriers.
+int ring_smem(int bn, int kb, int eg, int stages) { return 1024 + eg * 128 * bn + stages * (128 + bn) * kb + 256; }
+int epi_groups_for(int kb_per_tile) { return kb_per_tile <= 1 ? 2 : 1; }
+int ring_stages(int bn, int kb, int eg) {
+  return std::min(8, (227 * 1024 - kStaticSmem - 1024 - 256 - eg * 128 * bn) / ((128 + bn) * kb));
+}
+
 tzcdev::FastDiv make_fdiv(int64_t d) {
   tzcdev::FastDiv f{};
   f.d = (uint32_t)d;
@@ -126,15 +133,15 @@ cudaError_t launch_pdl(Kern kern, dim3 grid, dim3 block, size_t smem, cudaStream
 
 template <int BN, int KB, bool F16, int AM, bool BMN, int EPM>
 Status launch_kernel(const ConvKernelParams& p, int grid, cudaStream_t stream) {
-  using Cfg = ConvCfg<BN, KB>;
   auto kern = tzcdev::conv_tc_kernel<BN, KB, F16, AM, BMN, EPM>;
   static bool attr_done = false;  // per instantiation
   if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024 - kStaticSmem);
     if (e != cudaSuccess) return Status(TZC_E_DEVICE, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
     attr_done = true;
   }
-  cudaError_t e = launch_pdl(kern, dim3(grid), dim3(tzcdev::EpiCfg<BN>::THREADS), Cfg::SMEM_BYTES, stream, p);
+  const int smem = ring_smem(BN, KB, p.epi_groups, p.stages);
+  cudaError_t e = launch_pdl(kern, dim3(grid), dim3(tzcdev::EpiCfg<BN>::THREADS), smem, stream, p);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) return Status(TZC_E_DEVICE, std::string("conv_tc launch: ") + cudaGetErrorString(e));
@@ -340,13 +347,16 @@ Status plan_problem(const Problem& pb_in, tzc_plan* plan) {
   plan->bm = 128;
   plan->bn = bn;
   plan->bk_bytes = kb;
-  plan->stages = ent->stages;
+  // ping-pong epilogue groups where the epilogue dominates (one K block
+  // per tile); otherwise one group and the deepest ring
+  const int eg = epi_groups_for(num_kb / splits);
+  plan->stages = ring_stages(bn, kb, eg);
   plan->a_mode = pb.a_mode;
   plan->splits = splits;
   plan->tiles_m = tiles_m;
   plan->tiles_n = tiles_n;
   plan->grid = std::min(tiles * splits, sms);
-  plan->smem_bytes = ent->smem;
+  plan->smem_bytes = ring_smem(bn, kb, eg, plan->stages);
   plan->workspace_bytes = splits > 1 ? (int64_t)splits * M * pb.ngemm * 4 : 0;
   return Status();
 }
@@ -747,6 +757,8 @@ Status run_problem(const Problem& pb, const void* a, const void* b, const void* 
   p.tiles_n = plan.tiles_n;
   p.num_tiles = plan.tiles_m * plan.tiles_n;
   p.splits = plan.splits;
+  p.stages = plan.stages;
+  p.epi_groups = epi_groups_for(p.num_kb / plan.splits);
   p.fd_splits = make_fdiv(plan.splits);
   p.fd_tiles_n = make_fdiv(plan.tiles_n);
   p.fd_ohow = make_fdiv(std::max<int64_t>(1, (int64_t)pb.oh * pb.ow));

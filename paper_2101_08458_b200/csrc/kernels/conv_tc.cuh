@@ -125,6 +125,8 @@ struct alignas(64) ConvKernelParams {
   int32_t simple;              // requant, 2^-k (k>=2), no seed, no range check, row-major, aligned
   int32_t tma_store;           // int8 tile staged in SMEM, written by TMA (full-line stores)
   int32_t mt;                  // shifted-window: 128-row tiles per work unit
+  int32_t stages;              // general kernel: SMEM ring depth
+  int32_t epi_groups;          // general kernel: 1 or 2 (ping-pong) epilogue groups
   uint64_t magic_hw, magic_wp; // ceil(2^40 / (Hp*Wp)), ceil(2^40 / Wp): exact q / d for q < 2^22
   int32_t debug_flags;         // tools only: 1 = skip epilogue body, 2 = skip epilogue stores
   // shifted-window MMA table: per MMA of a channel block, the A start-address
@@ -143,11 +145,17 @@ struct ConvCfg {
   static constexpr int A_BYTES = BM * KB;
   static constexpr int B_BYTES = BN * KB;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES_RAW = (192 * 1024) / STAGE_BYTES;
-  static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
+  // int8 output tile(s) staged for the TMA store: 4 lane quarters x 32 rows x
+  // BN per epilogue group.  The ring depth is chosen at launch (p.stages):
+  // two staging tiles (ping-pong epilogue groups) leave fewer stages.
+  static constexpr int STAGING_BYTES = 128 * BN;  // one epilogue group
+  static constexpr int STAGES_FOR(int groups) {
+    return ((227 * 1024 - 1024 - 256 - groups * STAGING_BYTES) / STAGE_BYTES) > 8
+               ? 8
+               : (227 * 1024 - 1024 - 256 - groups * STAGING_BYTES) / STAGE_BYTES;
+  }
+  static constexpr int STAGES = STAGES_FOR(1);  // ring capacity (smem layout)
   static constexpr uint32_t TMEM_COLS = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128 : (2 * BN <= 256) ? 256 : 512;
-  // int8 output tile staged for the TMA store: 4 lane quarters x 32 rows x BN
-  static constexpr int STAGING_BYTES = 128 * BN;
   static constexpr int SMEM_BYTES = 1024 /*align slack*/ + STAGING_BYTES + STAGES * STAGE_BYTES + 256;
 };
 
@@ -430,7 +438,8 @@ template <int BN, int KB, bool kF16, int kAMode, bool kBMN, int kEpm>
 __global__ void __launch_bounds__(EpiCfg<BN>::THREADS, 1) conv_tc_kernel(const __grid_constant__ ConvKernelParams p) {
   using Cfg = ConvCfg<BN, KB>;
   constexpr int BM = Cfg::BM;
-  constexpr int STAGES = Cfg::STAGES;
+  const int STAGES = p.stages;       // host-chosen ring depth (<= 8)
+  const int EG = p.epi_groups;       // 1: 16 epilogue warps per tile; 2: ping-pong groups of 8
   constexpr int KE = kF16 ? KB / 2 : KB;  // K elements per block
   constexpr int MMAS = KB / 32;           // K=32 (i8) / K=16 (f16): 32 bytes per MMA
   constexpr uint32_t IDESC = kF16 ? idesc_f16(BM, BN, kBMN) : idesc_i8(BM, BN);
@@ -439,8 +448,8 @@ __global__ void __launch_bounds__(EpiCfg<BN>::THREADS, 1) conv_tc_kernel(const _
   TZC_TRACE_DECL
   TZC_TRACE_INIT;
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sStage = smem;  // TMA-store staging (1024-aligned, STAGING_BYTES)
-  uint8_t* sA = smem + Cfg::STAGING_BYTES;
+  uint8_t* sStage = smem;  // TMA-store staging: EG tiles of STAGING_BYTES (1024-aligned)
+  uint8_t* sA = smem + EG * Cfg::STAGING_BYTES;
   uint8_t* sB = sA + STAGES * Cfg::A_BYTES;
   uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * Cfg::B_BYTES);
   uint64_t* empty = full + STAGES;
@@ -463,7 +472,7 @@ __global__ void __launch_bounds__(EpiCfg<BN>::THREADS, 1) conv_tc_kernel(const _
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], EpiCfg<BN>::WARPS);
+      mbar_init(&tempty[a], 16 / EG);  // the warps that drain buffer a
     }
     fence_barrier_init();
   }
@@ -484,7 +493,7 @@ __global__ void __launch_bounds__(EpiCfg<BN>::THREADS, 1) conv_tc_kernel(const _
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int u = blockIdx.x; u < num_units; u += gridDim.x) {
+      for (int u = blockIdx.x, it = 0; u < num_units; u += gridDim.x, ++it) {
         const int tile = (int)fdiv(u, p.fd_splits), split = u - tile * p.splits;
         const int m_tile = (int)fdiv(tile, p.fd_tiles_n), n_tile = tile - m_tile * p.tiles_n;
         const int kb0 = (int)fdiv(split * p.num_kb, p.fd_splits);
@@ -497,7 +506,6 @@ __global__ void __launch_bounds__(EpiCfg<BN>::THREADS, 1) conv_tc_kernel(const _
           oh = (int)fdiv(rem, p.fd_ow);
           ow = rem - oh * p.OW;
         }
-        const int it = (u - (int)blockIdx.x) / (int)gridDim.x;
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           if (kb == kb0 && it < 10) TZC_TRACE_POINT(10 + 5 * it);
@@ -533,8 +541,7 @@ __global__ void __launch_bounds__(EpiCfg<BN>::THREADS, 1) conv_tc_kernel(const _
     uint32_t phase = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int u = blockIdx.x; u < num_units; u += gridDim.x) {
-      const int it = (u - (int)blockIdx.x) / (int)gridDim.x;
+    for (int u = blockIdx.x, it = 0; u < num_units; u += gridDim.x, ++it) {
       if (lane == 0 && it < 10) TZC_TRACE_POINT(80 + it);
       const int split = u - (int)fdiv(u, p.fd_splits) * p.splits;
       const int kb0 = (int)fdiv(split * p.num_kb, p.fd_splits);
@@ -580,33 +587,38 @@ __global__ void __launch_bounds__(EpiCfg<BN>::THREADS, 1) conv_tc_kernel(const _
     }
   } else if (warp >= 4) {
     // ===================== epilogue =====================
-    const uint32_t q = warp & 3;         // TMEM lane quarter this warp may access
-    const uint32_t h = (warp - 4) >> 2;  // column group
-    constexpr int HALF = EpiCfg<BN>::COLS;
-    int acc = 0;
+    // EG == 1: all 16 warps drain every tile (4 per TMEM lane quarter, BN/4
+    // columns each).  EG == 2 (thin-K layers, where the epilogue is the
+    // bottleneck): two groups of 8 warps ping-pong over the two accumulator
+    // buffers, so one group's tcgen05.ld / requant / store burst overlaps the
+    // other's instead of all 16 warps stalling on the same tile.
+    const uint32_t q = warp & 3;  // TMEM lane quarter this warp may access
+    const uint32_t g = EG == 2 ? (warp - 4) >> 3 : 0;
+    const uint32_t h = EG == 2 ? ((warp - 4) >> 2) & 1 : (warp - 4) >> 2;
+    const int HALF = BN / (4 / EG);              // columns per warp
+    constexpr int CW = EpiCfg<BN>::CW;           // min(BN/4, 32)
+    const uint32_t nthr = 32 * (4 / EG);         // named-barrier participants per lane quarter
+    int acc = (int)g;
     uint32_t acc_phase = 0;
-    for (int u = blockIdx.x; u < num_units; u += gridDim.x) {
+    for (int u = blockIdx.x + (int)g * (int)gridDim.x, it = (int)g; u < num_units; u += EG * gridDim.x, it += EG) {
       const int tile = (int)fdiv(u, p.fd_splits), split = u - tile * p.splits;
       const int m_tile = (int)fdiv(tile, p.fd_tiles_n), n_tile = tile - m_tile * p.tiles_n;
       const int m = m_tile * BM + q * 32 + lane;
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      const int it = (u - (int)blockIdx.x) / (int)gridDim.x;
       if (threadIdx.x == 128 && it < 10) TZC_TRACE_POINT(13 + 5 * it);
+      if (threadIdx.x == 128 + 256 && it < 10) TZC_TRACE_POINT(13 + 5 * it);
       // whole tile in range and 16-byte aligned: the compact vector epilogue;
       // otherwise (ragged channels, odd strides) the element-wise one
       const bool fast = p.vec_ok && (n_tile + 1) * BN <= p.Ngemm;
+      const uint32_t tq = tmem_base + ((q * 32) << 16) + acc * BN;
       if (p.debug_flags & 1) {
       } else if (p.ep_kind == EP_PARTIAL) {
-        constexpr int CW = EpiCfg<BN>::CW;
 #pragma unroll 1
         for (int c = 0; c < HALF / CW; ++c) {
           const int col = h * HALF + c * CW;
           uint32_t v[CW];
-          if constexpr (CW == 16)
-            tmem_ld16(tmem_base + ((q * 32) << 16) + acc * BN + col, v);
-          else
-            tmem_ld32(tmem_base + ((q * 32) << 16) + acc * BN + col, v);
+          tmem_ld_cw<CW>(tq + col, v);
           tmem_ld_wait();
           const int n = n_tile * BN + col;
           if (m < p.M) {
@@ -617,49 +629,50 @@ __global__ void __launch_bounds__(EpiCfg<BN>::THREADS, 1) conv_tc_kernel(const _
           }
         }
       } else if (kEpm == EPM_REQUANT && p.tma_store) {
-        // int8 tile -> SMEM staging (this lane quarter's 32 rows x BN) ->
-        // one TMA store per 128-byte column box: whole 128-byte output lines
-        // instead of 32 scattered 16-byte pieces per warp store.
-        constexpr int CW = EpiCfg<BN>::CW;
+        // int8 tile -> SMEM staging (this group's lane quarter: 32 rows x BN)
+        // -> one TMA store per 128-byte column box: whole 128-byte output
+        // lines instead of 32 scattered 16-byte pieces per warp store.
         constexpr int RB = BN < 128 ? BN : 128;
-        uint8_t* stq = sStage + q * (32 * BN);
-        if (h == 0 && lane == 0) bulk_wait_read0();  // previous tile's store has read the staging
-        named_bar_sync(1 + q, 32 * EpiCfg<BN>::GROUPS);
+        uint8_t* stq = sStage + g * (128 * BN) + q * (32 * BN);
+        const uint32_t bar = 1 + g * 4 + q;
+        if (h == 0 && lane == 0) bulk_wait_read0();  // this group's previous store has read the staging
+        named_bar_sync(bar, nthr);
 #pragma unroll 1
         for (int c = 0; c < HALF / CW; ++c) {
           const int col = h * HALF + c * CW;
-          epi_chunk<CW, kF16, kEpm, BN>(p, tmem_base + ((q * 32) << 16) + acc * BN + col,
-                                        (m < p.M && !(p.debug_flags & 2)) ? m : -1, n_tile * BN + col, true,
-                                        smem_u32(stq), (int)lane, col);
+          epi_chunk<CW, kF16, kEpm, BN>(p, tq + col, (m < p.M && !(p.debug_flags & 2)) ? m : -1, n_tile * BN + col,
+                                        true, smem_u32(stq), (int)lane, col);
         }
         fence_proxy_async_smem();
-        named_bar_sync(1 + q, 32 * EpiCfg<BN>::GROUPS);
+        named_bar_sync(bar, nthr);
         if (h == 0 && lane == 0) {
 #pragma unroll
           for (int b = 0; b < BN / RB; ++b) tma_store_2d(&p.tmO, stq + b * (32 * RB), n_tile * BN + b * RB, m_tile * BM + q * 32);
           bulk_commit();
         }
       } else {
-        constexpr int CW = EpiCfg<BN>::CW;
 #pragma unroll 1
         for (int c = 0; c < HALF / CW; ++c) {
           const int col = h * HALF + c * CW;
-          epi_chunk<CW, kF16, kEpm, BN>(p, tmem_base + ((q * 32) << 16) + acc * BN + col,
-                                        (m < p.M && !(p.debug_flags & 2)) ? m : -1, n_tile * BN + col, fast);
+          epi_chunk<CW, kF16, kEpm, BN>(p, tq + col, (m < p.M && !(p.debug_flags & 2)) ? m : -1, n_tile * BN + col,
+                                        fast);
         }
       }
       tc_fence_before();
       __syncwarp();
       if (threadIdx.x == 128 && it < 10) TZC_TRACE_POINT(14 + 5 * it);
-      if (lane == 0 && it < 10) TZC_TRACE_MAX(100 + it);
+      if (threadIdx.x == 128 + 256 && it < 10) TZC_TRACE_POINT(14 + 5 * it);
       if (lane == 0) mbar_arrive(&tempty[acc]);
-      if (++acc == 2) {
+      if (EG == 2) {
+        acc_phase ^= 1;
+      } else if (++acc == 2) {
         acc = 0;
         acc_phase ^= 1;
       }
     }
   }
-  if (kEpm == EPM_REQUANT && p.tma_store && warp >= 4 && ((warp - 4) >> 2) == 0 && lane == 0)
+  if (kEpm == EPM_REQUANT && p.tma_store && warp >= 4 && lane == 0 &&
+      (p.epi_groups == 2 ? (((warp - 4) >> 2) & 1) == 0 : ((warp - 4) >> 2) == 0))
     bulk_wait0();  // staged stores complete before the CTA (and its SMEM) retires
   __syncwarp();  // roles diverge within warps 0/1; bar.sync requires convergence
   __syncthreads();

@@ -108,9 +108,8 @@ __global__ void __launch_bounds__(EpiCfg<BN>::THREADS, 1) conv_ws_kernel(const _
       }
       int slot = 0;
       uint32_t phase = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      for (int tile = blockIdx.x, it = 0; tile < num_tiles; tile += gridDim.x, ++it) {
         const int q0 = tile * MT * BM;
-        const int it = (tile - (int)blockIdx.x) / (int)gridDim.x;
         for (int cb = 0; cb < c_blocks; ++cb) {
           mbar_wait(&aempty[slot], phase ^ 1);
           if (it < 10) TZC_TRACE_POINT(10 + 5 * it);
@@ -147,11 +146,10 @@ __global__ void __launch_bounds__(EpiCfg<BN>::THREADS, 1) conv_ws_kernel(const _
     uint32_t phase = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+    for (int tile = blockIdx.x, it = 0; tile < num_tiles; tile += gridDim.x, ++it) {
       mbar_wait(&tempty[acc], acc_phase ^ 1);
       tc_fence_after();
       const uint32_t tmem_acc = tmem_base + acc * (MT * BN);
-      const int it = (tile - (int)blockIdx.x) / (int)gridDim.x;
       if (lane == 0 && it < 10) TZC_TRACE_POINT(11 + 5 * it);
       for (int cb = 0; cb < c_blocks; ++cb) {
         mbar_wait(&afull[slot], phase);
@@ -211,10 +209,9 @@ __global__ void __launch_bounds__(EpiCfg<BN>::THREADS, 1) conv_ws_kernel(const _
     const int hw = p.Hp * p.Wp;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+    for (int tile = blockIdx.x, it = 0; tile < num_tiles; tile += gridDim.x, ++it) {
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      const int it = (tile - (int)blockIdx.x) / (int)gridDim.x;
       if (threadIdx.x == 128 && it < 10) TZC_TRACE_POINT(13 + 5 * it);
       {
         // 16 warps over MT tiles: G = 4 / MT column groups per tile, so warp

@@ -72,8 +72,16 @@ int main(int argc, char** argv) {
              (long long)(t[11 + 5 * i] - t[0]), (long long)(t[12 + 5 * i] - t[0]), (long long)(t[70 + i] - t[0]), (long long)(t[13 + 5 * i] - t[0]),
              (long long)(t[14 + 5 * i] - t[0]));
     for (int i = 0; i < 10; ++i)
-      printf("  tile %d: mmaLoopTop=%lld temptyOk=%lld lastEpiWarpEnd=%lld\n", i, (long long)(t[80 + i] - t[0]),
-             (long long)(t[90 + i] - t[0]), (long long)(t[100 + i] - t[0]));
+      printf("  tile %d: mmaLoopTop=%lld temptyOk=%lld lastEpiWarpEnd=%lld epiLoopTop=%lld\n", i, (long long)(t[80 + i] - t[0]),
+             (long long)(t[90 + i] - t[0]), (long long)(t[100 + i] - t[0]), (long long)(t[110 + i] - t[0]));
+  }
+  {
+    unsigned long long t[128];
+    tzc_trace_dump(t);
+    printf("  tile 5 epilogue (thread 128): start=%lld bar1=%lld chunk0=%lld chunk1=%lld chunk2=%lld bar2=%lld tma=%lld end=%lld\n",
+           (long long)(t[18 + 5 * 5 - 5] - t[0]), (long long)(t[120] - t[0]), (long long)(t[121] - t[0]),
+           (long long)(t[122] - t[0]), (long long)(t[123] - t[0]), (long long)(t[124] - t[0]), (long long)(t[125] - t[0]),
+           (long long)(t[14 + 5 * 5] - t[0]));
   }
   return 0;
 }
