@@ -221,6 +221,10 @@ int tzc_b200_set_option(const char* name, int64_t value) {
     set_ws_enabled(value ? 1 : 0);
     return TZC_OK;
   }
+  if (n == "ws_epi_groups") {
+    set_ws_epi_groups((int)value);
+    return TZC_OK;
+  }
   if (n == "tma_store") {
     set_tma_store(value ? 1 : 0);
     return TZC_OK;

@@ -5,6 +5,7 @@
 // exact reference program is served by one memory-bound gather pass.  Output
 // needs no adapter: the epilogue writes blocked layouts directly
 // (tzc_out_layout).  Byte moves only — bit-exact by construction.
+#include <algorithm>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -240,6 +241,29 @@ __global__ void s2d_data_kernel(const uint8_t* __restrict__ x, uint4* __restrict
   }
 }
 
+// C = 3 stem, one block per S2D row (n, h4): the two input rows are read
+// with coalesced 16-bit loads into shared memory, then every thread emits
+// 16-byte S2D pixels with one vector store.  Memory-bound; replaces the
+// per-pixel kernel's 64-bit index math and six scattered loads per pixel.
+__global__ void s2d_rows_c3_kernel(const uint8_t* __restrict__ x, uint4* __restrict__ x4, int Hp, int Wp, int Hp4,
+                                   int Wp4, int rows) {
+  // grid-stride over S2D rows (n, h4); thread t of the block emits pixels
+  // w4 = t, t + 128, ... with six independent 16-bit loads each (no shared
+  // memory round trip, 32-bit index math once per row)
+  for (int row = blockIdx.x; row < rows; row += gridDim.x) {
+    const int n = row / Hp4, h4 = row - n * Hp4;
+    const uint16_t* r0 = reinterpret_cast<const uint16_t*>(x + ((int64_t)n * Hp + 2 * h4) * Wp * 3);
+    const uint16_t* r1 = r0 + Wp * 3 / 2;  // Hp, Wp even (host): row 2*h4+1 exists, 2-byte aligned
+    uint4* dst = x4 + (int64_t)row * Wp4;
+#pragma unroll 2
+    for (int w4 = threadIdx.x; w4 < Wp4; w4 += blockDim.x) {
+      const uint32_t a0 = __ldg(r0 + 3 * w4), a1 = __ldg(r0 + 3 * w4 + 1), a2 = __ldg(r0 + 3 * w4 + 2);
+      const uint32_t b0 = __ldg(r1 + 3 * w4), b1 = __ldg(r1 + 3 * w4 + 1), b2 = __ldg(r1 + 3 * w4 + 2);
+      dst[w4] = make_uint4(a0 | (a1 << 16), a2 | (b0 << 16), b1 | (b2 << 16), 0u);
+    }
+  }
+}
+
 __global__ void zero_tail_kernel(uint4* p, int64_t from, int64_t to) {
   for (int64_t i = from + threadIdx.x; i < to; i += blockDim.x) p[i] = make_uint4(0, 0, 0, 0);
 }
@@ -271,8 +295,14 @@ namespace tzcb200 {
 Status s2d_stem(const Problem& pb, const void* x, const void* w, void* x4, void* w4, int hp4, int wp4, int r4, int s4,
                 cudaStream_t st) {
   const int64_t npix4 = (int64_t)pb.n * hp4 * wp4;
-  tzcdev::s2d_data_kernel<<<blocks_for(npix4), 256, 0, st>>>((const uint8_t*)x, (uint4*)x4, npix4, pb.hp, pb.wp, pb.c,
-                                                             hp4, wp4);
+  if (pb.c == 3 && pb.hp % 2 == 0 && pb.wp % 2 == 0 && reinterpret_cast<uintptr_t>(x) % 2 == 0) {
+    const int rows = pb.n * hp4;
+    tzcdev::s2d_rows_c3_kernel<<<std::min(rows, 148 * 16), 128, 0, st>>>((const uint8_t*)x, (uint4*)x4, pb.hp, pb.wp,
+                                                                         hp4, wp4, rows);
+  } else {
+    tzcdev::s2d_data_kernel<<<blocks_for(npix4), 256, 0, st>>>((const uint8_t*)x, (uint4*)x4, npix4, pb.hp, pb.wp, pb.c,
+                                                               hp4, wp4);
+  }
   g_launches.fetch_add(1, std::memory_order_relaxed);
   const int64_t padded = (npix4 + 7) / 8 * 8;
   if (padded > npix4) {

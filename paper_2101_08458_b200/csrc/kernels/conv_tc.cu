@@ -225,6 +225,7 @@ struct Scratch {
   size_t bytes[3] = {0, 0, 0};
 };
 std::map<cudaStream_t, Scratch> g_ws;
+int g_ws_epi_groups = 1;  // shifted-window epilogue groups (set_option "ws_epi_groups")
 int g_tma_store = 1;  // TMA-store int8 epilogue (set_option "tma_store")
 int g_forced_splits = 0;
 int g_ws_enabled = 1;  // shifted-window kernel for eligible stride-1 convs (TZC_B200_NO_WS=1 disables)
@@ -249,6 +250,7 @@ Status workspace(int slot, size_t bytes, void** out, cudaStream_t stream) {
 void set_forced_splits(int s) { g_forced_splits = s; }
 void set_ws_enabled(int on) { g_ws_enabled = on; }
 void set_tma_store(int on) { g_tma_store = on; }
+void set_ws_epi_groups(int g) { g_ws_epi_groups = g == 1 ? 1 : 2; }
 
 // ---- K7 (thin-channel) rewrite ------------------------------------------------
 bool needs_k7(const Problem& pb) { return pb.b_kn == 0 && ((int64_t)pb.c * (pb.f16 ? 2 : 1)) % 16 != 0; }
@@ -574,6 +576,7 @@ Status run_ws(const Problem& pb, const WsPlan& w, const void* a, const void* b, 
   p.num_tiles = w.tiles;
   p.splits = w.a_slots;  // ring depth (the kernel has no split-K)
   p.mt = w.mt;
+  p.epi_groups = g_ws_epi_groups;
   fill_epilogue(&p, pb, seed, out, ep);
   WsFn fn = ws_fn(w.bn, w.kb, pb.f16 != 0, w.pair != 0);
   if (!fn) return Status(TZC_E_INTERNAL, "no conv_ws instantiation");

@@ -81,7 +81,7 @@ __global__ void __launch_bounds__(EpiCfg<BN>::THREADS, 1) conv_ws_kernel(const _
     mbar_init(bfull, 1);
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], EpiCfg<BN>::WARPS);
+      mbar_init(&tempty[a], EpiCfg<BN>::WARPS / p.epi_groups);
     }
     fence_barrier_init();
   }
@@ -204,21 +204,28 @@ __global__ void __launch_bounds__(EpiCfg<BN>::THREADS, 1) conv_ws_kernel(const _
     }
   } else if (warp >= 4) {
     // ===================== epilogue: padded grid -> output rows =====================
+    // EG (p.epi_groups) groups of 16/EG warps; group g drains accumulator
+    // buffer g for EG == 2 (ping-pong over alternate units).  A group's W =
+    // 4/EG warps per TMEM lane quarter split the unit's MT tiles x BN columns:
+    // W >= MT: G = W/MT column groups per tile; W < MT: MT/W whole tiles each.
+    const int EG = p.epi_groups;
     const uint32_t q4 = warp & 3;
-    const uint32_t h = (warp - 4) >> 2;
+    const int W = 4 / EG;
+    const int g = EG == 2 ? (int)((warp - 4) >> 3) : 0;
+    const int h = (int)((warp - 4) >> 2) % W;
     const int hw = p.Hp * p.Wp;
-    int acc = 0;
+    const int G = W >= MT ? W / MT : 1;
+    const int TPW = W >= MT ? 1 : MT / W;  // tiles per warp
+    const int cols = BN / G, col0 = (h % G) * cols;
+    int acc = g;
     uint32_t acc_phase = 0;
-    for (int tile = blockIdx.x, it = 0; tile < num_tiles; tile += gridDim.x, ++it) {
+    for (int tile = blockIdx.x + g * (int)gridDim.x, it = g; tile < num_tiles; tile += EG * gridDim.x, it += EG) {
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       if (threadIdx.x == 128 && it < 10) TZC_TRACE_POINT(13 + 5 * it);
-      {
-        // 16 warps over MT tiles: G = 4 / MT column groups per tile, so warp
-        // (q4, h) owns tile h / G, columns (h % G) * BN / G ... — one row-decode
-        // per unit, and with MT = 4 whole output rows per thread (full sectors)
-        const int G = 4 / MT;
-        const int t = (int)h / G, cols = BN / G, col0 = ((int)h % G) * cols;
+#pragma unroll 1
+      for (int i = 0; i < TPW; ++i) {
+        const int t = W >= MT ? h / G : h * TPW + i;
         const int q = (tile * MT + t) * BM + q4 * 32 + lane;
         int m = -1;
         if (q < p.P) {  // exact magic-number division (q < 2^22 host-checked)
@@ -242,7 +249,9 @@ __global__ void __launch_bounds__(EpiCfg<BN>::THREADS, 1) conv_ws_kernel(const _
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);
       if (threadIdx.x == 128 && it < 10) TZC_TRACE_POINT(14 + 5 * it);
-      if (++acc == 2) {
+      if (EG == 2) {
+        acc_phase ^= 1;
+      } else if (++acc == 2) {
         acc = 0;
         acc_phase ^= 1;
       }

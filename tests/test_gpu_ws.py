@@ -45,7 +45,7 @@ def test_ws_conv_bitexact(cuda, n, hp, c, k, r):
     assert np.array_equal(q, Orc.requant_i8(Orc.conv2d_nhwc(x, w, 1), scale))
 
 
-@pytest.mark.parametrize("n,hp,k", [(2, 230, 64), (1, 62, 64), (3, 62, 128)])
+@pytest.mark.parametrize("n,hp,k", [(2, 230, 64), (1, 62, 64), (3, 62, 128), (2, 61, 64)])
 def test_s2d_stem_bitexact(cuda, n, hp, k):
     """7x7 stride-2 over C=3: space-to-depth to 16-byte pixels + the pair-mode kernel."""
     x = Orc.random_tensor("u8", (n, hp, hp, 3), 310)

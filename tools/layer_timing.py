@@ -18,7 +18,11 @@ ap = argparse.ArgumentParser()
 ap.add_argument("layers", nargs="+")
 ap.add_argument("--batch", type=int, default=256)
 ap.add_argument("--reps", type=int, default=8)
+ap.add_argument("--opt", action="append", default=[], help="name=value for tzc_b200_set_option")
 a = ap.parse_args()
+for o in a.opt:
+    k, v = o.split("=")
+    D.set_option(k, int(v))
 dev = torch.device("cuda:0")
 gen = torch.Generator(device=dev)
 gen.manual_seed(0)
