@@ -411,15 +411,17 @@ TensorizedOp tensorize(const ComputeOp& op, const Intrinsic& intr) {
 // ============================ execution ==================================
 namespace {
 
+// Per host thread: device staging buffers and streams, so concurrent
+// run_op calls from different threads (independent ops) overlap their
+// copies and kernels instead of serialising on one buffer set.
 struct DeviceBuf {
   void* p = nullptr;
   size_t bytes = 0;
 };
-std::mutex g_pool_mu;
-DeviceBuf g_pool[8];
+thread_local DeviceBuf t_pool[8];
 
 void* pool(int slot, size_t bytes) {
-  DeviceBuf& b = g_pool[slot];
+  DeviceBuf& b = t_pool[slot];
   if (bytes > b.bytes) {
     if (b.p) cudaFree(b.p);
     b.p = nullptr;
@@ -511,7 +513,6 @@ void run_tensorized_packed(const TensorizedOp& t, const std::map<std::string, co
     auto it = host.find(op.out);
     hs = it == host.end() ? nullptr : it->second;  // absent initial image => zeros
   }
-  std::lock_guard<std::mutex> lk(g_pool_mu);
   const size_t xb = td.size() * elem_bytes(td.dtype), wb = tw.size() * elem_bytes(tw.dtype);
   const size_t sb = to.size() * elem_bytes(to.dtype);
   void* dx = pool(0, xb);
@@ -579,8 +580,8 @@ void run_tensorized_packed(const TensorizedOp& t, const std::map<std::string, co
     if (p.family == KernelPlan::Family::Matmul) chunk = std::max<int64_t>(128, (chunk + 127) / 128 * 128);
   }
   if (chunk < units) {
-    static cudaStream_t S[3] = {nullptr, nullptr, nullptr};
-    static cudaEvent_t ev_w = nullptr;
+    thread_local cudaStream_t S[3] = {nullptr, nullptr, nullptr};
+    thread_local cudaEvent_t ev_w = nullptr;
     if (!S[0]) {
       for (auto& x : S) cuda_ok(cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking), "stream");
       cuda_ok(cudaEventCreateWithFlags(&ev_w, cudaEventDisableTiming), "event");
@@ -615,7 +616,8 @@ void run_tensorized_packed(const TensorizedOp& t, const std::map<std::string, co
     return;
   }
 
-  cudaStream_t st = nullptr;
+  thread_local cudaStream_t st = nullptr;  // non-blocking: no implicit sync with other threads' streams
+  if (!st) cuda_ok(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "stream");
   cuda_ok(cudaMemcpyAsync(dx, hx, xb, cudaMemcpyHostToDevice, st), "H2D data");
   cuda_ok(cudaMemcpyAsync(dw, hw, wb, cudaMemcpyHostToDevice, st), "H2D weight");
   if (hs) cuda_ok(cudaMemcpyAsync(ds, hs, sb, cudaMemcpyHostToDevice, st), "H2D accumulator image");

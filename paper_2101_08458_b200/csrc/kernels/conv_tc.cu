@@ -226,7 +226,8 @@ struct Scratch {
 };
 std::map<cudaStream_t, Scratch> g_ws;
 int g_ws_epi_groups = 1;  // shifted-window epilogue groups (set_option "ws_epi_groups")
-int g_tma_store = 1;  // TMA-store int8 epilogue (set_option "tma_store")
+int g_tma_store = 1;
+int g_forced_bn = 0;  // set_option "bn" (0 = automatic)  // TMA-store int8 epilogue (set_option "tma_store")
 int g_forced_splits = 0;
 int g_ws_enabled = 1;  // shifted-window kernel for eligible stride-1 convs (TZC_B200_NO_WS=1 disables)
 
@@ -250,6 +251,7 @@ Status workspace(int slot, size_t bytes, void** out, cudaStream_t stream) {
 void set_forced_splits(int s) { g_forced_splits = s; }
 void set_ws_enabled(int on) { g_ws_enabled = on; }
 void set_tma_store(int on) { g_tma_store = on; }
+void set_forced_bn(int bn) { g_forced_bn = (bn == 64 || bn == 128 || bn == 256) ? bn : 0; }
 void set_ws_epi_groups(int g) { g_ws_epi_groups = g == 1 ? 1 : 2; }
 
 // ---- K7 (thin-channel) rewrite ------------------------------------------------
@@ -330,6 +332,7 @@ Status plan_problem(const Problem& pb_in, tzc_plan* plan) {
   // binding resource for these layers (ncu: L2-throughput-bound at BN=64).
   int bn = pb.ngemm % 256 == 0 ? 256 : (pb.ngemm % 128 == 0 ? 128 : 64);
   if (pb.b_kn) bn = pb.ngemm % 128 == 0 ? 128 : 64;  // MN-major path instantiated for 64/128
+  if (g_forced_bn && pb.ngemm % g_forced_bn == 0 && !(pb.b_kn && g_forced_bn == 256)) bn = g_forced_bn;
   const int sms = num_sms();
   const int tiles_m = (int)((M + 127) / 128);
   const int tiles_n = (pb.ngemm + bn - 1) / bn;
