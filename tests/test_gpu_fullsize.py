@@ -68,3 +68,24 @@ def test_resnet50_layer_b32(cuda, layer):
             win = xn[:, r:r + L.stride * (o - 1) + 1:L.stride, c_:c_ + L.stride * (o - 1) + 1:L.stride, :]
             tot += int(win.astype(np.int64).sum((0, 1, 2)) @ wsum[r, c_])
     assert wrap32(int(out.astype(np.int64).sum())) == wrap32(tot)
+
+
+@pytest.mark.parametrize("layer", [L.name for L in RESNET50_V15])
+def test_resnet50_layer_f16_b64(cuda, layer):
+    """configs[3]: the fp16 suite at batch 64 with fp32 accumulation (kind::f16
+    MMAs, fp32 TMEM accumulators): the first and last images against the
+    oracle's fp16 conv (per-op fp32 rounding in declared order) within the
+    reference's compare() tolerance 1e-3; fp16-cast outputs on the same run."""
+    from tests.gpu_helpers import rel_dev
+    L = next(x for x in RESNET50_V15 if x.name == layer)
+    nb = 64
+    x = Orc.random_tensor("fp16", (nb, L.h, L.h, L.c), 900)
+    w = Orc.random_tensor("fp16", (L.k, L.r, L.r, L.c), 901)
+    xd, wd = to_dev(x, cuda, True), to_dev(w, cuda, True)
+    out = D.conv2d(xd, wd, L.stride, epilogue="f32").cpu().numpy()
+    h16 = D.conv2d(xd, wd, L.stride, epilogue="f16").cpu().numpy().astype(np.float32)
+    for img in (0, nb - 1):
+        ref = Orc.conv2d_nhwc(x[img:img + 1], w, L.stride, fp16=True)
+        assert rel_dev(ref, out[img:img + 1]) <= 1e-3, f"image {img}"
+        assert rel_dev(ref, h16[img:img + 1]) <= 1e-3, f"image {img} (fp16 cast)"
+    assert np.isfinite(out).all()

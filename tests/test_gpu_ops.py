@@ -90,3 +90,25 @@ def test_run_op_errors(cuda):
         ops.run_op(text, "tcgen05_i8_m128n64k32", ins, epilogue="tensor Z : i32 [2] input\ntensor Q : i8 [2] output\n"
                    "loop i : dp 2\nQ[i] = cast<i8>(Z[i])\n")
     assert e.value.kind == "InjectError"
+
+
+def test_run_op_concurrent_threads(cuda):
+    """Independent ops from several host threads (per-thread device buffers
+    and streams in the library) stay exact."""
+    from concurrent.futures import ThreadPoolExecutor
+    cases = []
+    for i, (n, h, c, k, r, st) in enumerate([(3, 12, 64, 64, 3, 1), (2, 21, 3, 64, 7, 2), (4, 9, 128, 256, 1, 1),
+                                              (5, 10, 64, 128, 3, 2)]):
+        text = conv2d_nhwc_tdsl(n, h, h, c, k, r, r, st)
+        ins = Orc.random_inputs(decls(text), 40 + i)
+        cases.append((text, ins, Orc.conv2d_nhwc(ins["data"], ins["kernel"], st, ins["out"])))
+
+    def run(case):
+        text, ins, _ = case
+        return [ops.run_op(text, "tcgen05_i8_m128n64k32", ins) for _ in range(3)]
+
+    with ThreadPoolExecutor(4) as ex:
+        results = list(ex.map(run, cases))
+    for (text, ins, ref), outs in zip(cases, results):
+        for got in outs:
+            assert np.array_equal(got, ref)
