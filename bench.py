@@ -37,6 +37,8 @@ sys.path.insert(0, ROOT)
 
 METRIC = "ResNet-50 int8 conv-layer TOPS & % tcgen05 i8 peak at 1/2/4/8 B200"
 SPEC_I8_TOPS = 4500.0
+SPEC_F16_TFLOPS = 2250.0
+METRIC_F16 = "ResNet-50 fp16 conv-layer TFLOPS (configs[3], fp32 accumulation) & % tcgen05 f16 peak"
 
 
 def parse():
@@ -47,6 +49,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--batch", type=int, default=256, help="global batch, sharded over the ranks")
     ap.add_argument("--layers", default="", help="comma list of layer names (default: all 23)")
+    ap.add_argument("--profile", default="i8", choices=["i8", "f16"],
+                    help="i8: the BASELINE metric (default); f16: configs[3] (fp16 in, fp32 accumulate, fp16 out)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-threads", type=int, default=3, help="host threads issuing run_op calls in the e2e leg")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -174,16 +178,23 @@ class Cudart:
         return f.value
 
 
-def build_suite(torch, dev, batch, names, gen):
+def build_suite(torch, dev, batch, names, gen, profile="i8"):
     from paper_2101_08458_b200.workloads import RESNET50_V15, requant_scale
     layers = [L for L in RESNET50_V15 if not names or L.name in names]
     bufs = []
     for L in layers:
         o = L.out_hw()
-        x = torch.randint(0, 256, (batch, L.h, L.h, L.c), dtype=torch.uint8, device=dev, generator=gen)
-        w = torch.randint(-128, 128, (L.k, L.r, L.r, L.c), dtype=torch.int8, device=dev, generator=gen)
-        out = torch.empty((batch, o, o, L.k), dtype=torch.int8, device=dev)
-        bufs.append({"layer": L, "x": x, "w": w, "out": out, "scale": requant_scale(L.c * L.r * L.r)})
+        if profile == "f16":  # configs[3]: fp16 U[0,1) inputs, fp32 accumulation, fp16-cast output
+            x = torch.rand((batch, L.h, L.h, L.c), device=dev, generator=gen).half()
+            w = torch.rand((L.k, L.r, L.r, L.c), device=dev, generator=gen).half()
+            out = torch.empty((batch, o, o, L.k), dtype=torch.float16, device=dev)
+            bufs.append({"layer": L, "x": x, "w": w, "out": out, "scale": 1.0, "ep": "f16"})
+        else:
+            x = torch.randint(0, 256, (batch, L.h, L.h, L.c), dtype=torch.uint8, device=dev, generator=gen)
+            w = torch.randint(-128, 128, (L.k, L.r, L.r, L.c), dtype=torch.int8, device=dev, generator=gen)
+            out = torch.empty((batch, o, o, L.k), dtype=torch.int8, device=dev)
+            bufs.append({"layer": L, "x": x, "w": w, "out": out, "scale": requant_scale(L.c * L.r * L.r),
+                         "ep": "requant_i8"})
     return layers, bufs
 
 
@@ -200,9 +211,10 @@ def run_ours(args, rank, world, local):
     gen = torch.Generator(device=dev)
     gen.manual_seed(1234 + rank)
     bpg = shard_batch(args.batch, world)  # images on this rank
-    layers, bufs = build_suite(torch, dev, bpg, names, gen)
+    layers, bufs = build_suite(torch, dev, bpg, names, gen, args.profile)
+    eb = 2 if args.profile == "f16" else 1
     ops_step = sum(L.ops(bpg) for L in layers)
-    bytes_step = sum(L.algo_bytes(bpg) for L in layers)
+    bytes_step = sum(L.algo_bytes(bpg, eb, eb) for L in layers)
     stream = torch.cuda.Stream(device=dev)
     flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device=dev)
     rt = Cudart()
@@ -212,7 +224,7 @@ def run_ours(args, rank, world, local):
         for i, b in enumerate(bufs):
             if record:
                 rt.record(evs[i], stream)
-            D.conv2d(b["x"], b["w"], b["layer"].stride, epilogue="requant_i8", scale=b["scale"],
+            D.conv2d(b["x"], b["w"], b["layer"].stride, epilogue=b["ep"], scale=b["scale"],
                      out=b["out"], stream=stream)
         if record:
             rt.record(evs[len(bufs)], stream)
@@ -231,7 +243,7 @@ def run_ours(args, rank, world, local):
             bs.wait_event(fork)
             for i in order[k::len(branch_streams)]:
                 b = bufs[i]
-                D.conv2d(b["x"], b["w"], b["layer"].stride, epilogue="requant_i8", scale=b["scale"],
+                D.conv2d(b["x"], b["w"], b["layer"].stride, epilogue=b["ep"], scale=b["scale"],
                          out=b["out"], stream=bs)
             e = torch.cuda.Event()
             e.record(bs)
@@ -301,20 +313,23 @@ def run_ours(args, rank, world, local):
     value = job_tops(ops_step, world, ms_step)  # TOPS, whole job
 
     pk = peaks()
+    f16 = args.profile == "f16"
+    spec = SPEC_F16_TFLOPS if f16 else SPEC_I8_TOPS
+    tpeak = pk["bf16_tflops"] if f16 else pk["i8_tops"]
     layer_rows = []
     for b, v in zip(bufs, per_layer):
         L = b["layer"]
         ms = statistics.median(v)
         ops = L.ops(bpg)
-        by = L.algo_bytes(bpg)
-        roof = min(SPEC_I8_TOPS, ops / by * pk["hbm_gbs"] / 1e3)
+        by = L.algo_bytes(bpg, eb, eb)
+        roof = min(spec, ops / by * pk["hbm_gbs"] / 1e3)
         layer_rows.append({"layer": L.name, "ms": ms, "tops": ops / (ms * 1e-3) / 1e12,
                            "gbs": by / (ms * 1e-3) / 1e9, "roofline_tops_spec": roof,
                            "plan": plan_of(D, b)})
     result = {
-        "metric": METRIC,
+        "metric": METRIC_F16 if f16 else METRIC,
         "value": round(value, 2),
-        "unit": "TOPS",
+        "unit": "TFLOPS" if f16 else "TOPS",
         "n_gpus": world,
         "steps": args.steps,
         "warmup": args.warmup,
@@ -322,16 +337,18 @@ def run_ours(args, rank, world, local):
         "higher_is_better": True,
         "scaling": "strong",
         "vs_baseline": None,
-        "dtype": "u8xi8->i32 (requant i8 out)",
-        "data": "synthetic (uniform u8 activations / i8 weights, torch.Generator seeded per rank)",
-        "config": {"workload": "resnet50_v1.5_int8_conv_suite (23 distinct shapes, SURVEY.md App. A)",
+        "dtype": "f16xf16->f32 (f16 out)" if f16 else "u8xi8->i32 (requant i8 out)",
+        "data": ("synthetic (fp16 U[0,1) activations and weights, torch.Generator seeded per rank)" if f16 else
+                 "synthetic (uniform u8 activations / i8 weights, torch.Generator seeded per rank)"),
+        "config": {"workload": ("resnet50_v1.5_fp16_conv_suite (23 distinct shapes, configs[3])" if f16 else
+                                "resnet50_v1.5_int8_conv_suite (23 distinct shapes, SURVEY.md App. A)"),
                    "batch_per_gpu": bpg, "global_batch": args.batch,
                    "layers": len(layers), "ops_per_step_per_gpu": ops_step,
                    "algo_bytes_per_step_per_gpu": bytes_step,
                    "l2": "flushed (512 MiB memset) between timed steps, outside the timed events",
                    "parallelism": f"dp{world} (batch-sharded, no collective)",
                    "graph_branches": args.branches},
-        "pct_of_spec_i8_peak": round(100.0 * value / (SPEC_I8_TOPS * world), 2),
+        "pct_of_spec_peak": round(100.0 * value / (spec * world), 2),
         "gpu_launches": launches_per_step * args.steps,
         "clocks": clk.summary(),
     }
@@ -344,30 +361,31 @@ def run_ours(args, rank, world, local):
     # same L2-flush protocol, right after the timed region)
     dom = max(layer_rows, key=lambda r: r["ms"])
     dL = next(L for L in layers if L.name == dom["layer"])
-    hbm_bound = dom["roofline_tops_spec"] < SPEC_I8_TOPS
+    hbm_bound = dom["roofline_tops_spec"] < spec
     if hbm_bound:
-        ach, peak, unit = dL.algo_bytes(bpg) / (dom["ms"] * 1e-3) / 1e9, pk["hbm_gbs"], "GB/s"
+        ach, peak, unit = dL.algo_bytes(bpg, eb, eb) / (dom["ms"] * 1e-3) / 1e9, pk["hbm_gbs"], "GB/s"
     else:
-        ach, peak, unit = dom["tops"], pk["i8_tops"], "TFLOP/s"
+        ach, peak, unit = dom["tops"], tpeak, "TFLOP/s"
     result["roofline"] = {
         "bound": "hbm" if hbm_bound else "tensor",
         "kernel": f"{dom['layer']} ({kernel_name(dom.get('plan', {}))})",
         "achieved": round(ach, 2), "peak": round(peak, 1), "unit": unit, "frac": round(ach / peak, 4),
         "peak_basis": (f"HBM copy bandwidth, {pk['source']}" if hbm_bound else
-                       f"2 x bf16 burst, {pk['source']}; spec dense i8 = {SPEC_I8_TOPS}"),
-        "algorithmic_per_launch": {"bytes": dL.algo_bytes(bpg), "ops": dL.ops(bpg)},
+                       (f"bf16 burst, {pk['source']}; spec dense fp16 = {spec}" if f16 else
+                        f"2 x bf16 burst, {pk['source']}; spec dense i8 = {spec}")),
+        "algorithmic_per_launch": {"bytes": dL.algo_bytes(bpg, eb, eb), "ops": dL.ops(bpg)},
         "share_of_step": round(dom["ms"] / kern_ms, 4),
         "traffic": traffic_from_profiles(dom["layer"]),
-        "suite": {"bound": "tensor", "achieved": round(suite_achieved, 2), "peak": round(pk["i8_tops"], 1),
-                  "unit": "TFLOP/s", "frac": round(suite_achieved / pk["i8_tops"], 4),
-                  "frac_of_spec": round(suite_achieved / SPEC_I8_TOPS, 4),
+        "suite": {"bound": "tensor", "achieved": round(suite_achieved, 2), "peak": round(tpeak, 1),
+                  "unit": "TFLOP/s", "frac": round(suite_achieved / tpeak, 4),
+                  "frac_of_spec": round(suite_achieved / spec, 4),
                   "cold_hbm_ceiling_frac_of_spec": round(
                       ops_step / sum(L.ops(bpg) / r["roofline_tops_spec"] for L, r in zip(layers, layer_rows))
-                      / SPEC_I8_TOPS, 4)},
+                      / spec, 4)},
     }
-    if not args.no_e2e:
+    if not args.no_e2e and not f16:
         result["e2e"] = run_e2e(args, torch, D, bufs, stream, ops_step, world, dist)
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and not f16:
         result["cpu_baseline"] = cpu_baseline(args.cpu_seconds, layers)
     if args.layer_table and rank == 0:
         with open(args.layer_table, "w") as f:
