@@ -398,7 +398,8 @@ def run_ours(args, rank, world, local):
 
 def plan_of(D, b):
     L = b["layer"]
-    d, _ = D.conv_desc(tuple(b["x"].shape), tuple(b["w"].shape), L.stride)
+    import torch
+    d, _ = D.conv_desc(tuple(b["x"].shape), tuple(b["w"].shape), L.stride, f16=b["x"].dtype == torch.float16)
     try:
         return D.plan_conv(d)
     except Exception as e:  # noqa: BLE001
