@@ -226,8 +226,9 @@ struct Scratch {
 };
 std::map<cudaStream_t, Scratch> g_ws;
 int g_ws_epi_groups = 1;  // shifted-window epilogue groups (set_option "ws_epi_groups")
-int g_tma_store = 1;
-int g_forced_bn = 0;  // set_option "bn" (0 = automatic)  // TMA-store int8 epilogue (set_option "tma_store")
+int g_tma_store = 1;   // TMA-store int8 epilogue (set_option "tma_store")
+int g_forced_bn = 0;   // set_option "bn" (0 = automatic)
+int g_ws_1x1 = 0;      // set_option "ws_1x1": force the weight-stationary kernel for every 1x1 stride-1 conv
 int g_forced_splits = 0;
 int g_ws_enabled = 1;  // shifted-window kernel for eligible stride-1 convs (TZC_B200_NO_WS=1 disables)
 
@@ -251,6 +252,7 @@ Status workspace(int slot, size_t bytes, void** out, cudaStream_t stream) {
 void set_forced_splits(int s) { g_forced_splits = s; }
 void set_ws_enabled(int on) { g_ws_enabled = on; }
 void set_tma_store(int on) { g_tma_store = on; }
+void set_ws_1x1(int on) { g_ws_1x1 = on ? 1 : 0; }
 void set_forced_bn(int bn) { g_forced_bn = (bn == 64 || bn == 128 || bn == 256) ? bn : 0; }
 void set_ws_epi_groups(int g) { g_ws_epi_groups = g == 1 ? 1 : 2; }
 
@@ -447,7 +449,11 @@ WsFn ws_fn(int bn, int kb, bool f16, bool pair) {
 // Eligibility + resources of the shifted-window kernel for a stride-1 conv
 // (pair = 16-byte pixels, the space-to-depth stem).
 bool ws_plan(const Problem& pb, bool pair, WsPlan* w) {
-  if (pb.b_kn || pb.stride != 1 || pb.taps < 2 || needs_k7(pb)) return false;
+  if (pb.b_kn || pb.stride != 1 || needs_k7(pb)) return false;
+  // 1x1: weight-stationary pays off only for a single 64-wide N tile and one
+  // K block (c2_1x1_64_64: 43 -> 31 us at batch 256); wider layers keep the
+  // TMA-store general kernel (measured, tools/layer_timing.py --opt ws_1x1=1)
+  if (pb.taps < 2 && !g_ws_1x1 && !(pb.ngemm == 64 && (int64_t)pb.c * (pb.f16 ? 2 : 1) <= 128)) return false;
   if (!(pb.ngemm == 64 || pb.ngemm == 128 || pb.ngemm == 256)) return false;
   const int e = pb.f16 ? 2 : 1;
   const int64_t cb = (int64_t)pb.c * e;
