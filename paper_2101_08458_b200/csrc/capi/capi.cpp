@@ -225,6 +225,10 @@ int tzc_b200_set_option(const char* name, int64_t value) {
     set_ws_epi_groups((int)value);
     return TZC_OK;
   }
+  if (n == "tail_split") {
+    set_tail_split((int)value);
+    return TZC_OK;
+  }
   if (n == "ws_1x1") {
     set_ws_1x1((int)value);
     return TZC_OK;

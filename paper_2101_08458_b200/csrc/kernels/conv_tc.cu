@@ -37,6 +37,49 @@ constexpr int kStaticSmem = 0;
 // General-kernel SMEM: EG int8 staging tiles (128 x BN) + the A/B ring + barriers.
 int ring_smem(int bn, int kb, int eg, int stages) { return 1024 + eg * 128 * bn + stages * (128 + bn) * kb + 256; }
 int epi_groups_for(int kb_per_tile) { return kb_per_tile <= 1 ? 2 : 1; }
+
+// How the tiles are cut along K.  none: every unit a whole tile.  classic
+// split-K (fewer tiles than SMs): every tile split.  tail split: the last,
+// less-than-half-full round of tiles is split `splits` ways, so it costs
+// ~1/splits of a round instead of a whole one (c5 layers: 196 tiles on 148
+// SMs).  Whole tiles keep the fused epilogue; split ones go through the
+// int32 fix-up kernel, exact because wrapping adds are associative.
+struct WorkSplit {
+  int splits = 1;
+  int full = 0;  // whole-tile units (they come first)
+};
+int g_tail_split = 0;  // set_option "tail_split" (measured slower with the separate fix-up kernel)
+WorkSplit work_split(int tiles, int tiles_n, int num_kb, int sms, bool ok16, int forced) {
+  WorkSplit w;
+  w.full = tiles;
+  if (forced > 0) {
+    w.splits = std::min(forced, num_kb);
+    w.full = w.splits > 1 ? 0 : tiles;
+    return w;
+  }
+  if (!ok16) return w;
+  if (tiles < sms) {
+    // fill the machine, keeping >= 8 K blocks per split so the int32 partial
+    // round trip stays small next to the MMA work
+    const int s = std::min((sms + tiles - 1) / tiles, num_kb / 8);
+    if (s >= 2) {
+      w.splits = s;
+      w.full = 0;
+    }
+    return w;
+  }
+  const int tail = tiles % sms;
+  if (g_tail_split && tail > 0 && 2 * tail <= sms && num_kb >= 8) {
+    int full = tiles - tail;
+    full -= full % tiles_n;  // the split region starts on an M-tile boundary
+    const int s = std::min(num_kb / 4, sms / (tiles - full));
+    if (s >= 2) {
+      w.splits = s;
+      w.full = full;
+    }
+  }
+  return w;
+}
 int ring_stages(int bn, int kb, int eg) {
   return std::min(8, (227 * 1024 - kStaticSmem - 1024 - 256 - eg * 128 * bn) / ((128 + bn) * kb));
 }
@@ -150,7 +193,7 @@ Status launch_kernel(const ConvKernelParams& p, int grid, cudaStream_t stream) {
 
 template <bool F16, int EPM>
 Status launch_reduce(const ConvKernelParams& p, cudaStream_t stream) {
-  int64_t groups = (int64_t)p.M * (p.Ngemm / 16);
+  int64_t groups = (int64_t)p.red_rows * (p.Ngemm / 16);
   int blocks = (int)std::min<int64_t>((groups + 255) / 256, 4 * 148);
   cudaError_t e = launch_pdl(tzcdev::splitk_reduce_kernel<F16, EPM>, dim3(blocks), dim3(256), 0, stream, p);
   g_launches.fetch_add(1, std::memory_order_relaxed);
@@ -167,10 +210,18 @@ Status launch_impl(const ConvKernelParams& p, int grid, cudaStream_t stream) {
                   : (p.ep_kind == tzcdev::EP_CAST_F16) ? tzcdev::EPM_F16
                                                        : tzcdev::EPM_RAW;
   constexpr int kAlt = F16 ? tzcdev::EPM_F16 : tzcdev::EPM_REQUANT;
-  if (p.splits > 1) {
+  if (p.splits > 1 && p.full_units == 0) {  // classic split-K: every unit writes partials
     ConvKernelParams pk = p;
     pk.ep_kind = tzcdev::EP_PARTIAL;  // raw partials; the fix-up applies the epilogue
     Status st = launch_kernel<BN, KB, F16, AM, BMN, tzcdev::EPM_RAW>(pk, grid, stream);
+    if (!st.ok()) return st;
+    return epm == tzcdev::EPM_RAW ? launch_reduce<F16, tzcdev::EPM_RAW>(p, stream) : launch_reduce<F16, kAlt>(p, stream);
+  }
+  if (p.splits > 1) {  // tail split: whole tiles finish in-kernel, the split tail in the fix-up
+    Status st = epm == tzcdev::EPM_RAW ? launch_kernel<BN, KB, F16, AM, BMN, tzcdev::EPM_RAW>(p, grid, stream)
+                                       : ((epm == tzcdev::EPM_F16) != F16
+                                              ? Status(TZC_E_TYPE, "epilogue kind does not match the profile")
+                                              : launch_kernel<BN, KB, F16, AM, BMN, kAlt>(p, grid, stream));
     if (!st.ok()) return st;
     return epm == tzcdev::EPM_RAW ? launch_reduce<F16, tzcdev::EPM_RAW>(p, stream) : launch_reduce<F16, kAlt>(p, stream);
   }
@@ -250,6 +301,7 @@ Status workspace(int slot, size_t bytes, void** out, cudaStream_t stream) {
 }  // namespace
 
 void set_forced_splits(int s) { g_forced_splits = s; }
+void set_tail_split(int on) { g_tail_split = on ? 1 : 0; }
 void set_ws_enabled(int on) { g_ws_enabled = on; }
 void set_tma_store(int on) { g_tma_store = on; }
 void set_ws_1x1(int on) { g_ws_1x1 = on ? 1 : 0; }
@@ -340,15 +392,9 @@ Status plan_problem(const Problem& pb_in, tzc_plan* plan) {
   const int tiles_n = (pb.ngemm + bn - 1) / bn;
   const int num_kb = (int)(pb.taps * ((krow_bytes + kb - 1) / kb));
   const int tiles = tiles_m * tiles_n;
-  int splits = 1;
-  if (g_forced_splits > 0) {
-    splits = std::min(g_forced_splits, num_kb);
-  } else if (tiles < sms && pb.ngemm % 16 == 0) {
-    // split the reduction to fill the machine, but keep >= 8 K blocks per
-    // split so the int32 partial round trip stays small next to the MMA work
-    splits = std::min((sms + tiles - 1) / tiles, num_kb / 8);
-    if (splits < 2) splits = 1;
-  }
+  const WorkSplit wsplit = work_split(tiles, tiles_n, num_kb, sms, pb.ngemm % 16 == 0, g_forced_splits);
+  const int splits = wsplit.splits;
+  const int64_t red_m0 = (int64_t)(wsplit.full / tiles_n) * 128;
   const Entry* ent = find_entry(bn, kb, pb.f16, pb.a_mode, pb.b_kn);
   if (!ent) return Status(TZC_E_INTERNAL, "no kernel instantiation for this plan");
   plan->bm = 128;
@@ -362,9 +408,9 @@ Status plan_problem(const Problem& pb_in, tzc_plan* plan) {
   plan->splits = splits;
   plan->tiles_m = tiles_m;
   plan->tiles_n = tiles_n;
-  plan->grid = std::min(tiles * splits, sms);
+  plan->grid = std::min(wsplit.full + (tiles - wsplit.full) * splits, sms);
   plan->smem_bytes = ring_smem(bn, kb, eg, plan->stages);
-  plan->workspace_bytes = splits > 1 ? (int64_t)splits * M * pb.ngemm * 4 : 0;
+  plan->workspace_bytes = splits > 1 ? (int64_t)splits * (M - red_m0) * pb.ngemm * 4 : 0;
   return Status();
 }
 
@@ -769,6 +815,13 @@ Status run_problem(const Problem& pb, const void* a, const void* b, const void* 
   p.tiles_n = plan.tiles_n;
   p.num_tiles = plan.tiles_m * plan.tiles_n;
   p.splits = plan.splits;
+  {
+    const WorkSplit wsplit = work_split(p.num_tiles, plan.tiles_n, p.num_kb, num_sms(), pb.ngemm % 16 == 0,
+                                        g_forced_splits);
+    p.full_units = wsplit.full;
+    p.red_m0 = (int32_t)((wsplit.full / plan.tiles_n) * 128);
+    p.red_rows = (int32_t)(pb.m - p.red_m0);
+  }
   p.stages = plan.stages;
   p.epi_groups = epi_groups_for(p.num_kb / plan.splits);
   p.fd_splits = make_fdiv(plan.splits);
@@ -778,7 +831,7 @@ Status run_problem(const Problem& pb, const void* a, const void* b, const void* 
   p.fd_cblocks = make_fdiv(std::max(1, p.c_blocks));
   p.fd_s = make_fdiv(std::max(1, pb.s));
   fill_epilogue(&p, pb, seed, out, ep);
-  if (ep.kind == tzcdev::EP_REQUANT_I8 && plan.splits == 1 && p.vec_ok && pb.out.nb == pb.ngemm &&
+  if (ep.kind == tzcdev::EP_REQUANT_I8 && p.full_units > 0 && p.vec_ok && pb.out.nb == pb.ngemm &&
       pb.out.stride_m == pb.ngemm && pb.ngemm % plan.bn == 0 && g_tma_store) {
     // int8 output as a [M, Ngemm] map; one box = 32 rows x min(BN, 128) bytes
     const int rb = std::min(plan.bn, 128);

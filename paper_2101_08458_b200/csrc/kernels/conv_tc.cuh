@@ -126,6 +126,11 @@ struct alignas(64) ConvKernelParams {
   int32_t tma_store;           // int8 tile staged in SMEM, written by TMA (full-line stores)
   int32_t mt;                  // shifted-window: 128-row tiles per work unit
   int32_t stages;              // general kernel: SMEM ring depth
+  // work split: units [0, full_units) are whole tiles; the remaining tiles
+  // are split `splits` ways along K, their int32 partials stored at rows
+  // [red_m0, red_m0 + red_rows) of the workspace and combined by the fix-up
+  // kernel (classic split-K: full_units = 0; no split: full_units = num_tiles)
+  int32_t full_units, red_m0, red_rows;
   int32_t epi_groups;          // general kernel: 1 or 2 (ping-pong) epilogue groups
   uint64_t magic_hw, magic_wp; // ceil(2^40 / (Hp*Wp)), ceil(2^40 / Wp): exact q / d for q < 2^22
   int32_t debug_flags;         // tools only: 1 = skip epilogue body, 2 = skip epilogue stores
@@ -434,6 +439,24 @@ __device__ __forceinline__ void epi_chunk(const ConvKernelParams& p, uint32_t ta
   epi_regs<CW, kF16, kEpm, BN>(p, v, m, n, fast, stg, srow, scol);
 }
 
+// Work unit u -> (tile, split, K-block range); split = -1 for a whole tile.
+__device__ __forceinline__ void unit_decode(const ConvKernelParams& p, int u, int& tile, int& split, int& kb0,
+                                            int& kb1) {
+  if (u < p.full_units) {
+    tile = u;
+    split = -1;
+    kb0 = 0;
+    kb1 = p.num_kb;
+    return;
+  }
+  const int v = u - p.full_units;
+  const int t = (int)fdiv(v, p.fd_splits);
+  tile = p.full_units + t;
+  split = v - t * p.splits;
+  kb0 = (int)fdiv(split * p.num_kb, p.fd_splits);
+  kb1 = (int)fdiv((split + 1) * p.num_kb, p.fd_splits);
+}
+
 template <int BN, int KB, bool kF16, int kAMode, bool kBMN, int kEpm>
 __global__ void __launch_bounds__(EpiCfg<BN>::THREADS, 1) conv_tc_kernel(const __grid_constant__ ConvKernelParams p) {
   using Cfg = ConvCfg<BN, KB>;
@@ -486,7 +509,7 @@ __global__ void __launch_bounds__(EpiCfg<BN>::THREADS, 1) conv_tc_kernel(const _
   pdl_launch_dependents();
   pdl_wait();
 
-  const int num_units = p.num_tiles * p.splits;
+  const int num_units = p.full_units + (p.num_tiles - p.full_units) * p.splits;
 
   if (warp == 0) {
     // ===================== TMA producer =====================
@@ -494,10 +517,9 @@ __global__ void __launch_bounds__(EpiCfg<BN>::THREADS, 1) conv_tc_kernel(const _
       int stage = 0;
       uint32_t phase = 0;
       for (int u = blockIdx.x, it = 0; u < num_units; u += gridDim.x, ++it) {
-        const int tile = (int)fdiv(u, p.fd_splits), split = u - tile * p.splits;
+        int tile, split, kb0, kb1;
+        unit_decode(p, u, tile, split, kb0, kb1);
         const int m_tile = (int)fdiv(tile, p.fd_tiles_n), n_tile = tile - m_tile * p.tiles_n;
-        const int kb0 = (int)fdiv(split * p.num_kb, p.fd_splits);
-        const int kb1 = (int)fdiv((split + 1) * p.num_kb, p.fd_splits);
         const int m0 = m_tile * BM, n0 = n_tile * BN;
         int img = 0, oh = 0, ow = 0;
         if constexpr (kAMode == A_IM2COL) {
@@ -543,9 +565,8 @@ __global__ void __launch_bounds__(EpiCfg<BN>::THREADS, 1) conv_tc_kernel(const _
     uint32_t acc_phase = 0;
     for (int u = blockIdx.x, it = 0; u < num_units; u += gridDim.x, ++it) {
       if (lane == 0 && it < 10) TZC_TRACE_POINT(80 + it);
-      const int split = u - (int)fdiv(u, p.fd_splits) * p.splits;
-      const int kb0 = (int)fdiv(split * p.num_kb, p.fd_splits);
-      const int kb1 = (int)fdiv((split + 1) * p.num_kb, p.fd_splits);
+      int tile, split, kb0, kb1;
+      unit_decode(p, u, tile, split, kb0, kb1);
       mbar_wait(&tempty[acc], acc_phase ^ 1);
       if (lane == 0 && it < 10) TZC_TRACE_POINT(90 + it);
       tc_fence_after();
@@ -601,7 +622,8 @@ __global__ void __launch_bounds__(EpiCfg<BN>::THREADS, 1) conv_tc_kernel(const _
     int acc = (int)g;
     uint32_t acc_phase = 0;
     for (int u = blockIdx.x + (int)g * (int)gridDim.x, it = (int)g; u < num_units; u += EG * gridDim.x, it += EG) {
-      const int tile = (int)fdiv(u, p.fd_splits), split = u - tile * p.splits;
+      int tile, split, kb0, kb1;
+      unit_decode(p, u, tile, split, kb0, kb1);
       const int m_tile = (int)fdiv(tile, p.fd_tiles_n), n_tile = tile - m_tile * p.tiles_n;
       const int m = m_tile * BM + q * 32 + lane;
       mbar_wait(&tfull[acc], acc_phase);
@@ -613,7 +635,7 @@ __global__ void __launch_bounds__(EpiCfg<BN>::THREADS, 1) conv_tc_kernel(const _
       const bool fast = p.vec_ok && (n_tile + 1) * BN <= p.Ngemm;
       const uint32_t tq = tmem_base + ((q * 32) << 16) + acc * BN;
       if (p.debug_flags & 1) {
-      } else if (p.ep_kind == EP_PARTIAL) {
+      } else if (split >= 0) {  // K-split unit: raw partial sums for the fix-up kernel
 #pragma unroll 1
         for (int c = 0; c < HALF / CW; ++c) {
           const int col = h * HALF + c * CW;
@@ -622,7 +644,7 @@ __global__ void __launch_bounds__(EpiCfg<BN>::THREADS, 1) conv_tc_kernel(const _
           tmem_ld_wait();
           const int n = n_tile * BN + col;
           if (m < p.M) {
-            uint32_t* o = static_cast<uint32_t*>(p.partial) + ((int64_t)split * p.M + m) * p.Ngemm + n;
+            uint32_t* o = static_cast<uint32_t*>(p.partial) + ((int64_t)split * p.red_rows + (m - p.red_m0)) * p.Ngemm + n;
 #pragma unroll
             for (int j = 0; j < CW / 4; ++j)
               if (n + 4 * j < p.Ngemm) st_v4(o + 4 * j, v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
@@ -691,16 +713,17 @@ template <bool kF16, int kEpm>
 __global__ void splitk_reduce_kernel(const __grid_constant__ ConvKernelParams p) {
   pdl_launch_dependents();
   pdl_wait();
-  const int64_t groups = (int64_t)p.M * (p.Ngemm / 16);
+  const int64_t groups = (int64_t)p.red_rows * (p.Ngemm / 16);
   for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < groups;
        g += (int64_t)gridDim.x * blockDim.x) {
-    const int m = (int)(g / (p.Ngemm / 16));
-    const int n = (int)(g - (int64_t)m * (p.Ngemm / 16)) * 16;
+    const int ml = (int)(g / (p.Ngemm / 16));  // row within the split region
+    const int m = p.red_m0 + ml;
+    const int n = (int)(g - (int64_t)ml * (p.Ngemm / 16)) * 16;
     uint32_t v[16];
     for (int i = 0; i < 16; ++i) v[i] = 0;
     for (int s = 0; s < p.splits; ++s) {
-      const uint4* src =
-          reinterpret_cast<const uint4*>(static_cast<const uint32_t*>(p.partial) + ((int64_t)s * p.M + m) * p.Ngemm + n);
+      const uint4* src = reinterpret_cast<const uint4*>(static_cast<const uint32_t*>(p.partial) +
+                                                        ((int64_t)s * p.red_rows + ml) * p.Ngemm + n);
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         uint4 t = ld_v4(src + j);

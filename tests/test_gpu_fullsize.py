@@ -89,3 +89,31 @@ def test_resnet50_layer_f16_b64(cuda, layer):
         assert rel_dev(ref, out[img:img + 1]) <= 1e-3, f"image {img}"
         assert rel_dev(ref, h16[img:img + 1]) <= 1e-3, f"image {img} (fp16 cast)"
     assert np.isfinite(out).all()
+
+
+@pytest.mark.parametrize("layer", ["c5_3x3_512", "c5_1x1_2048_512"])
+def test_tail_split_b256(cuda, layer):
+    """196 tiles on 148 SMs: the last round's tiles are split along K (int32
+    partials + fix-up) while whole tiles keep the fused epilogue.  Images from
+    the whole-tile region and from the split tail, int32 and requant."""
+    L = next(x for x in RESNET50_V15 if x.name == layer)
+    nb = 256
+    g = torch.Generator(device=cuda)
+    g.manual_seed(11)
+    x = torch.randint(0, 256, (nb, L.h, L.h, L.c), dtype=torch.uint8, device=cuda, generator=g)
+    w = torch.randint(-128, 128, (L.k, L.r, L.r, L.c), dtype=torch.int8, device=cuda, generator=g)
+    D.set_option("tail_split", 1)
+    try:
+        d, _ = D.conv_desc(tuple(x.shape), tuple(w.shape), L.stride)
+        plan = D.plan_conv(d)
+        assert plan["splits"] > 1 and plan["grid"] == 148, plan
+        out = D.conv2d(x, w, L.stride).cpu().numpy()
+        s = requant_scale(L.c * L.r * L.r)
+        q = D.conv2d(x, w, L.stride, epilogue="requant_i8", scale=s).cpu().numpy()
+    finally:
+        D.set_option("tail_split", 0)
+    xn, wn = x.cpu().numpy(), w.cpu().numpy()
+    for img in (0, 150, 200, nb - 1):  # rows 7350.. (whole tiles) and >= 9472 (split tail)
+        ref = Orc.conv2d_nhwc(xn[img:img + 1], wn, L.stride)
+        assert np.array_equal(out[img:img + 1], ref), f"image {img}"
+        assert np.array_equal(q[img:img + 1], Orc.requant_i8(ref, s)), f"image {img} (requant)"
