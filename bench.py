@@ -38,6 +38,7 @@ sys.path.insert(0, ROOT)
 METRIC = "ResNet-50 int8 conv-layer TOPS & % tcgen05 i8 peak at 1/2/4/8 B200"
 SPEC_I8_TOPS = 4500.0
 SPEC_F16_TFLOPS = 2250.0
+WRITE_GBS = 3870.0  # measured write-only HBM bandwidth (fill), tools/hbm_probe.py
 METRIC_F16 = "ResNet-50 fp16 conv-layer TFLOPS (configs[3], fp32 accumulation) & % tcgen05 f16 peak"
 
 
@@ -374,6 +375,14 @@ def run_ours(args, rank, world, local):
                        (f"bf16 burst, {pk['source']}; spec dense fp16 = {spec}" if f16 else
                         f"2 x bf16 burst, {pk['source']}; spec dense i8 = {spec}")),
         "algorithmic_per_launch": {"bytes": dL.algo_bytes(bpg, eb, eb), "ops": dL.ops(bpg)},
+        # direction-aware HBM floor: writes alone top out at ~3870 GB/s on this
+        # pool (fill, tools/hbm_probe.py) vs 6552 GB/s for a read+write copy
+        "hbm_floor_us": round(1e6 * max(dL.algo_bytes(bpg, eb, eb) / (pk["hbm_gbs"] * 1e9),
+                                        bpg * dL.out_hw() ** 2 * dL.k * eb / (WRITE_GBS * 1e9),
+                                        dL.ops(bpg) / (spec * 1e12)), 2),
+        "frac_of_hbm_floor": round(1e6 * max(dL.algo_bytes(bpg, eb, eb) / (pk["hbm_gbs"] * 1e9),
+                                             bpg * dL.out_hw() ** 2 * dL.k * eb / (WRITE_GBS * 1e9),
+                                             dL.ops(bpg) / (spec * 1e12)) / (dom["ms"] * 1e3), 4),
         "share_of_step": round(dom["ms"] / kern_ms, 4),
         "traffic": traffic_from_profiles(dom["layer"]),
         "suite": {"bound": "tensor", "achieved": round(suite_achieved, 2), "peak": round(tpeak, 1),
