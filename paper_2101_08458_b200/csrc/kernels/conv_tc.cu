@@ -279,6 +279,7 @@ std::map<cudaStream_t, Scratch> g_ws;
 int g_ws_epi_groups = 1;  // shifted-window epilogue groups (set_option "ws_epi_groups")
 int g_tma_store = 1;   // TMA-store int8 epilogue (set_option "tma_store")
 int g_forced_bn = 0;   // set_option "bn" (0 = automatic)
+int g_ws_mt = 0;       // set_option "ws_mt": force the shifted-window tiles per unit (0 = automatic)
 int g_ws_1x1 = 0;      // set_option "ws_1x1": force the weight-stationary kernel for every 1x1 stride-1 conv
 int g_forced_splits = 0;
 int g_ws_enabled = 1;  // shifted-window kernel for eligible stride-1 convs (TZC_B200_NO_WS=1 disables)
@@ -305,6 +306,7 @@ void set_tail_split(int on) { g_tail_split = on ? 1 : 0; }
 void set_ws_enabled(int on) { g_ws_enabled = on; }
 void set_tma_store(int on) { g_tma_store = on; }
 void set_ws_1x1(int on) { g_ws_1x1 = on ? 1 : 0; }
+void set_ws_mt(int mt) { g_ws_mt = (mt == 1 || mt == 2 || mt == 4) ? mt : 0; }
 void set_forced_bn(int bn) { g_forced_bn = (bn == 64 || bn == 128 || bn == 256) ? bn : 0; }
 void set_ws_epi_groups(int g) { g_ws_epi_groups = g == 1 ? 1 : 2; }
 
@@ -530,6 +532,7 @@ bool ws_plan(const Problem& pb, bool pair, WsPlan* w) {
   // busy for >= 8 units and loses <= 6% to the last round's imbalance
   for (int mt : {4, 2, 1}) {
     if (2 * mt * x.bn > 512) continue;
+    if (g_ws_mt && mt != g_ws_mt) continue;
     const int units = (tiles + mt - 1) / mt;
     if (mt > 1) {
       if (units < 8 * sms) continue;
@@ -631,6 +634,9 @@ Status run_ws(const Problem& pb, const WsPlan& w, const void* a, const void* b, 
   p.num_tiles = w.tiles;
   p.splits = w.a_slots;  // ring depth (the kernel has no split-K)
   p.mt = w.mt;
+  // as many accumulators as TMEM holds (<= 4): the epilogue may lag the MMAs
+  // by NACC-1 units (the ping-pong epilogue groups need exactly 2)
+  p.nacc = g_ws_epi_groups == 2 ? 2 : std::min(4, 512 / (w.mt * w.bn));
   p.epi_groups = g_ws_epi_groups;
   fill_epilogue(&p, pb, seed, out, ep);
   WsFn fn = ws_fn(w.bn, w.kb, pb.f16 != 0, w.pair != 0);

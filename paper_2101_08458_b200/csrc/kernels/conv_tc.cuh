@@ -125,6 +125,7 @@ struct alignas(64) ConvKernelParams {
   int32_t simple;              // requant, 2^-k (k>=2), no seed, no range check, row-major, aligned
   int32_t tma_store;           // int8 tile staged in SMEM, written by TMA (full-line stores)
   int32_t mt;                  // shifted-window: 128-row tiles per work unit
+  int32_t nacc;                // shifted-window: TMEM accumulators in flight (2 or 4)
   int32_t stages;              // general kernel: SMEM ring depth
   // work split: units [0, full_units) are whole tiles; the remaining tiles
   // are split `splits` ways along K, their int32 partials stored at rows

@@ -63,8 +63,9 @@ __global__ void __launch_bounds__(EpiCfg<BN>::THREADS, 1) conv_ws_kernel(const _
   uint64_t* aempty = afull + a_slots;
   uint64_t* bfull = aempty + a_slots;
   uint64_t* tfull = bfull + 1;
-  uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* tempty = tfull + 4;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 4);
+  const int NACC = p.nacc;  // TMEM accumulator ring: NACC x MT x BN <= 512 columns
 
   const uint32_t warp = warp_id();
   const uint32_t lane = threadIdx.x & 31;
@@ -79,7 +80,7 @@ __global__ void __launch_bounds__(EpiCfg<BN>::THREADS, 1) conv_ws_kernel(const _
       mbar_init(&aempty[s], 1);
     }
     mbar_init(bfull, 1);
-    for (int a = 0; a < 2; ++a) {
+    for (int a = 0; a < NACC; ++a) {
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], EpiCfg<BN>::WARPS / p.epi_groups);
     }
@@ -197,7 +198,7 @@ __global__ void __launch_bounds__(EpiCfg<BN>::THREADS, 1) conv_ws_kernel(const _
           phase ^= 1;
         }
       }
-      if (++acc == 2) {
+      if (++acc == NACC) {
         acc = 0;
         acc_phase ^= 1;
       }
@@ -251,7 +252,7 @@ __global__ void __launch_bounds__(EpiCfg<BN>::THREADS, 1) conv_ws_kernel(const _
       if (threadIdx.x == 128 && it < 10) TZC_TRACE_POINT(14 + 5 * it);
       if (EG == 2) {
         acc_phase ^= 1;
-      } else if (++acc == 2) {
+      } else if (++acc == NACC) {
         acc = 0;
         acc_phase ^= 1;
       }
