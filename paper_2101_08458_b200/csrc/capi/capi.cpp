@@ -229,6 +229,10 @@ int tzc_b200_set_option(const char* name, int64_t value) {
     set_tail_split((int)value);
     return TZC_OK;
   }
+  if (n == "pingpong_kb") {
+    set_pingpong_kb((int)value);
+    return TZC_OK;
+  }
   if (n == "ws_mt") {
     set_ws_mt((int)value);
     return TZC_OK;

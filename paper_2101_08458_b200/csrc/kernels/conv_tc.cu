@@ -36,7 +36,8 @@ constexpr int kStaticSmem = 0;
 #endif
 // General-kernel SMEM: EG int8 staging tiles (128 x BN) + the A/B ring + barriers.
 int ring_smem(int bn, int kb, int eg, int stages) { return 1024 + eg * 128 * bn + stages * (128 + bn) * kb + 256; }
-int epi_groups_for(int kb_per_tile) { return kb_per_tile <= 1 ? 2 : 1; }
+int g_pingpong_kb = 2;  // set_option "pingpong_kb": max K blocks per tile for ping-pong epilogue groups
+int epi_groups_for(int kb_per_tile) { return kb_per_tile <= g_pingpong_kb ? 2 : 1; }
 
 // How the tiles are cut along K.  none: every unit a whole tile.  classic
 // split-K (fewer tiles than SMs): every tile split.  tail split: the last,
@@ -306,6 +307,7 @@ void set_tail_split(int on) { g_tail_split = on ? 1 : 0; }
 void set_ws_enabled(int on) { g_ws_enabled = on; }
 void set_tma_store(int on) { g_tma_store = on; }
 void set_ws_1x1(int on) { g_ws_1x1 = on ? 1 : 0; }
+void set_pingpong_kb(int kb) { g_pingpong_kb = kb; }
 void set_ws_mt(int mt) { g_ws_mt = (mt == 1 || mt == 2 || mt == 4) ? mt : 0; }
 void set_forced_bn(int bn) { g_forced_bn = (bn == 64 || bn == 128 || bn == 256) ? bn : 0; }
 void set_ws_epi_groups(int g) { g_ws_epi_groups = g == 1 ? 1 : 2; }
