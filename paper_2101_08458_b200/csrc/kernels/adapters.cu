@@ -264,12 +264,33 @@ __global__ void s2d_rows_c3_kernel(const uint8_t* __restrict__ x, uint4* __restr
   }
 }
 
+// fp16 C = 3 stem: 32-byte S2D pixels (halfs (a*2+b)*3+c, 4 zero halfs);
+// the input pixel pair (2*w4, 2*w4+1) of a row is 12 contiguous bytes at a
+// 4-byte aligned offset (Wp even): three 32-bit loads per row.
+__global__ void s2d_rows_c3_f16_kernel(const uint8_t* __restrict__ x, uint4* __restrict__ x4, int Hp, int Wp, int Hp4,
+                                       int Wp4, int rows) {
+  for (int row = blockIdx.x; row < rows; row += gridDim.x) {
+    const int n = row / Hp4, h4 = row - n * Hp4;
+    const uint32_t* r0 = reinterpret_cast<const uint32_t*>(x + ((int64_t)n * Hp + 2 * h4) * Wp * 6);
+    const uint32_t* r1 = r0 + Wp * 3 / 2;
+    uint4* dst = x4 + (int64_t)row * Wp4 * 2;
+#pragma unroll 2
+    for (int w4 = threadIdx.x; w4 < Wp4; w4 += blockDim.x) {
+      const uint32_t a0 = __ldg(r0 + 3 * w4), a1 = __ldg(r0 + 3 * w4 + 1), a2 = __ldg(r0 + 3 * w4 + 2);
+      const uint32_t b0 = __ldg(r1 + 3 * w4), b1 = __ldg(r1 + 3 * w4 + 1), b2 = __ldg(r1 + 3 * w4 + 2);
+      dst[2 * w4] = make_uint4(a0, a1, a2, b0);
+      dst[2 * w4 + 1] = make_uint4(b1, b2, 0u, 0u);
+    }
+  }
+}
+
 __global__ void zero_tail_kernel(uint4* p, int64_t from, int64_t to) {
   for (int64_t i = from + threadIdx.x; i < to; i += blockDim.x) p[i] = make_uint4(0, 0, 0, 0);
 }
 
-__global__ void s2d_weight_kernel(const uint8_t* __restrict__ w, uint8_t* __restrict__ w4, int K, int R, int S, int C,
-                                  int64_t wsk, int64_t wst, int R4, int S4) {
+template <typename T>
+__global__ void s2d_weight_kernel(const T* __restrict__ w, T* __restrict__ w4, int K, int R, int S, int C, int64_t wsk,
+                                  int64_t wst, int R4, int S4) {
   const int64_t total = (int64_t)K * R4 * S4 * 16;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     const int ch = (int)(i % 16);
@@ -278,7 +299,7 @@ __global__ void s2d_weight_kernel(const uint8_t* __restrict__ w, uint8_t* __rest
     t /= S4;
     const int ii = (int)(t % R4);
     const int k = (int)(t / R4);
-    uint8_t v = 0;
+    T v = 0;
     if (ch < 4 * C) {
       const int ab = ch / C, c = ch - ab * C;
       const int r = 2 * ii + ab / 2, s = 2 * j + ab % 2;
@@ -295,7 +316,11 @@ namespace tzcb200 {
 Status s2d_stem(const Problem& pb, const void* x, const void* w, void* x4, void* w4, int hp4, int wp4, int r4, int s4,
                 cudaStream_t st) {
   const int64_t npix4 = (int64_t)pb.n * hp4 * wp4;
-  if (pb.c == 3 && pb.hp % 2 == 0 && pb.wp % 2 == 0 && reinterpret_cast<uintptr_t>(x) % 2 == 0) {
+  if (pb.f16) {  // C = 3, even extents (s2d_eligible)
+    const int rows = pb.n * hp4;
+    tzcdev::s2d_rows_c3_f16_kernel<<<std::min(rows, 148 * 16), 128, 0, st>>>((const uint8_t*)x, (uint4*)x4, pb.hp,
+                                                                             pb.wp, hp4, wp4, rows);
+  } else if (pb.c == 3 && pb.hp % 2 == 0 && pb.wp % 2 == 0 && reinterpret_cast<uintptr_t>(x) % 2 == 0) {
     const int rows = pb.n * hp4;
     tzcdev::s2d_rows_c3_kernel<<<std::min(rows, 148 * 16), 128, 0, st>>>((const uint8_t*)x, (uint4*)x4, pb.hp, pb.wp,
                                                                          hp4, wp4, rows);
@@ -305,13 +330,20 @@ Status s2d_stem(const Problem& pb, const void* x, const void* w, void* x4, void*
   }
   g_launches.fetch_add(1, std::memory_order_relaxed);
   const int64_t padded = (npix4 + 7) / 8 * 8;
-  if (padded > npix4) {
+  if (padded > npix4 && !pb.f16) {  // fp16 pixels are 32 B: the tail is zeroed as 2 uint4 each below
     tzcdev::zero_tail_kernel<<<1, 32, 0, st>>>((uint4*)x4, npix4, padded);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+  } else if (padded > npix4) {
+    tzcdev::zero_tail_kernel<<<1, 32, 0, st>>>((uint4*)x4, 2 * npix4, 2 * padded);
     g_launches.fetch_add(1, std::memory_order_relaxed);
   }
   const int64_t nw = (int64_t)pb.ngemm * r4 * s4 * 16;
-  tzcdev::s2d_weight_kernel<<<blocks_for(nw), 256, 0, st>>>((const uint8_t*)w, (uint8_t*)w4, pb.ngemm, pb.r, pb.s, pb.c,
-                                                            pb.w_stride_k, pb.w_stride_tap, r4, s4);
+  if (pb.f16)
+    tzcdev::s2d_weight_kernel<uint16_t><<<blocks_for(nw), 256, 0, st>>>(
+        (const uint16_t*)w, (uint16_t*)w4, pb.ngemm, pb.r, pb.s, pb.c, pb.w_stride_k, pb.w_stride_tap, r4, s4);
+  else
+    tzcdev::s2d_weight_kernel<uint8_t><<<blocks_for(nw), 256, 0, st>>>(
+        (const uint8_t*)w, (uint8_t*)w4, pb.ngemm, pb.r, pb.s, pb.c, pb.w_stride_k, pb.w_stride_tap, r4, s4);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? Status() : Status(TZC_E_DEVICE, cudaGetErrorString(e));

@@ -355,7 +355,7 @@ Status plan_problem(const Problem& pb_in, tzc_plan* plan) {
     const bool s2d = needs_k7(pb_in) && s2d_eligible(pb_in);
     const Problem q = s2d ? s2d_problem(pb_in) : pb_in;
     WsPlan w;
-    if ((s2d || (!needs_k7(pb_in) && g_ws_enabled)) && ws_plan(q, s2d, &w)) {
+    if ((s2d || (!needs_k7(pb_in) && g_ws_enabled)) && ws_plan(q, s2d && !pb_in.f16, &w)) {
       plan->bm = 128 * w.mt;  // rows per work unit
       plan->bn = w.bn;
       plan->bk_bytes = w.kb;
@@ -366,7 +366,7 @@ Status plan_problem(const Problem& pb_in, tzc_plan* plan) {
       plan->smem_bytes = w.smem;
       plan->tiles_m = w.tiles;
       plan->tiles_n = 1;
-      plan->workspace_bytes = s2d ? (int64_t)q.n * q.hp * q.wp * 16 : 0;
+      plan->workspace_bytes = s2d ? (int64_t)q.n * q.hp * q.wp * 16 * (pb_in.f16 ? 2 : 1) : 0;
       return Status();
     }
   }
@@ -490,6 +490,7 @@ WsFn ws_fn(int bn, int kb, bool f16, bool pair) {
   TZC_WS(64, 16, false, true) TZC_WS(128, 16, false, true) TZC_WS(256, 16, false, true)
   TZC_WS(64, 64, true, false) TZC_WS(128, 64, true, false) TZC_WS(256, 64, true, false)
   TZC_WS(64, 128, true, false) TZC_WS(128, 128, true, false) TZC_WS(256, 128, true, false)
+  TZC_WS(64, 32, true, false) TZC_WS(128, 32, true, false) TZC_WS(256, 32, true, false)
 #undef TZC_WS
   return nullptr;
 }
@@ -515,7 +516,7 @@ bool ws_plan(const Problem& pb, bool pair, WsPlan* w) {
     if (cb != 16 || pb.r != 4 || pb.s != 4 || pb.f16) return false;
     x.kb = 16;
   } else {
-    x.kb = cb % 128 == 0 ? 128 : (cb % 64 == 0 ? 64 : 0);
+    x.kb = cb % 128 == 0 ? 128 : (cb % 64 == 0 ? 64 : (pb.f16 && cb == 32 ? 32 : 0));  // 32: the fp16 S2D stem
     if (!x.kb) return false;
   }
   x.c_blocks = (int)(cb / x.kb);
@@ -564,6 +565,7 @@ Status run_ws(const Problem& pb, const WsPlan& w, const void* a, const void* b, 
   const CUtensorMapDataType dt = pb.f16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_UINT8;
   const CUtensorMapSwizzle sw = w.kb == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
                                 : w.kb == 64  ? CU_TENSOR_MAP_SWIZZLE_64B
+                                : w.kb == 32  ? CU_TENSOR_MAP_SWIZZLE_32B
                                               : CU_TENSOR_MAP_SWIZZLE_NONE;
   ConvKernelParams p;
   std::memset(&p, 0, sizeof(p));
@@ -647,9 +649,12 @@ Status run_ws(const Problem& pb, const WsPlan& w, const void* a, const void* b, 
 }
 
 // Space-to-depth geometry for a stride-2 conv with 4*C*e <= 16 (the stem).
+// int8: 16-byte S2D pixels (pair mode); fp16: C = 3 only (12 of 16 halfs per
+// 32-byte pixel, one K=16 MMA per tap), even padded extents.
 bool s2d_eligible(const Problem& pb) {
-  return pb.stride == 2 && !pb.f16 && !pb.b_kn && pb.c * 4 <= 16 && pb.r > 1 &&
-         (pb.ngemm == 64 || pb.ngemm == 128 || pb.ngemm == 256);
+  if (pb.stride != 2 || pb.b_kn || pb.r <= 1 || !(pb.ngemm == 64 || pb.ngemm == 128 || pb.ngemm == 256)) return false;
+  if (pb.f16) return pb.c == 3 && pb.hp % 2 == 0 && pb.wp % 2 == 0;
+  return pb.c * 4 <= 16;
 }
 
 Problem s2d_problem(const Problem& pb) {
@@ -719,11 +724,12 @@ Status run_problem(const Problem& pb, const void* a, const void* b, const void* 
     // kernel in pair mode (two taps per K=32 MMA)
     const Problem q = s2d_problem(pb);
     WsPlan w;
-    if (ws_plan(q, true, &w)) {
+    if (ws_plan(q, !pb.f16, &w)) {
       void* x4 = nullptr;
       void* w4 = nullptr;
-      st = workspace(1, (size_t)(((int64_t)q.n * q.hp * q.wp + 7) / 8 * 8) * 16, &x4, stream);
-      if (st.ok()) st = workspace(2, (size_t)q.ngemm * q.taps * 16, &w4, stream);
+      const int eb = pb.f16 ? 2 : 1;
+      st = workspace(1, (size_t)(((int64_t)q.n * q.hp * q.wp + 7) / 8 * 8) * 16 * eb, &x4, stream);
+      if (st.ok()) st = workspace(2, (size_t)q.ngemm * q.taps * 16 * eb, &w4, stream);
       if (st.ok()) st = s2d_stem(pb, a, b, x4, w4, q.hp, q.wp, q.r, q.s, stream);
       if (st.ok()) st = run_ws(q, w, x4, w4, seed, out, ep, stream);
       return st;

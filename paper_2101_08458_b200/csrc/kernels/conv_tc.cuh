@@ -659,20 +659,25 @@ __global__ void __launch_bounds__(EpiCfg<BN>::THREADS, 1) conv_tc_kernel(const _
         uint8_t* stq = sStage + g * (128 * BN) + q * (32 * BN);
         const uint32_t bar = 1 + g * 4 + q;
         if (h == 0 && lane == 0) bulk_wait_read0();  // this group's previous store has read the staging
+        if (threadIdx.x == 128 && it == 4) TZC_TRACE_POINT(119);
         named_bar_sync(bar, nthr);
+        if (threadIdx.x == 128 && it == 4) TZC_TRACE_POINT(120);
 #pragma unroll 1
         for (int c = 0; c < HALF / CW; ++c) {
           const int col = h * HALF + c * CW;
           epi_chunk<CW, kF16, kEpm, BN>(p, tq + col, (m < p.M && !(p.debug_flags & 2)) ? m : -1, n_tile * BN + col,
                                         true, smem_u32(stq), (int)lane, col);
+          if (threadIdx.x == 128 && it == 4 && c < 4) TZC_TRACE_POINT(121 + c);
         }
         fence_proxy_async_smem();
         named_bar_sync(bar, nthr);
+        if (threadIdx.x == 128 && it == 4) TZC_TRACE_POINT(125);
         if (h == 0 && lane == 0) {
 #pragma unroll
           for (int b = 0; b < BN / RB; ++b) tma_store_2d(&p.tmO, stq + b * (32 * RB), n_tile * BN + b * RB, m_tile * BM + q * 32);
           bulk_commit();
         }
+        if (threadIdx.x == 128 && it == 4) TZC_TRACE_POINT(126);
       } else {
 #pragma unroll 1
         for (int c = 0; c < HALF / CW; ++c) {

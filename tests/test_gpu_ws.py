@@ -102,3 +102,18 @@ def test_ws_requant_tiny_images(cuda, n, hp, c, k, r):
             finally:
                 D.set_option("tma_store", 1)
             assert np.array_equal(got, want), (scale, tma)
+
+
+@pytest.mark.parametrize("n,hp,k", [(2, 230, 64), (3, 62, 128), (2, 62, 256)])
+def test_s2d_stem_f16(cuda, n, hp, k):
+    """fp16 7x7 stride-2 stem over C=3: space-to-depth to 32-byte pixels and
+    the shifted-window kernel with one K=16 MMA per tap (SWIZZLE_32B)."""
+    x = Orc.random_tensor("fp16", (n, hp, hp, 3), 340)
+    w = Orc.random_tensor("fp16", (k, 7, 7, 3), 341)
+    d, _ = D.conv_desc((n, hp, hp, 3), (k, 7, 7, 3), 2, f16=True)
+    assert D.plan_conv(d)["a_mode"] == 3
+    ref = Orc.conv2d_nhwc(x, w, 2, fp16=True)
+    assert rel_dev(ref, run(cuda, x, w, 2, epilogue="f32")) <= 1e-3
+    o = (hp - 7) // 2 + 1
+    s0 = Orc.random_tensor("fp32", (n, o, o, k), 342)
+    assert rel_dev(Orc.conv2d_nhwc(x, w, 2, s0, fp16=True), run(cuda, x, w, 2, s0, epilogue="f32")) <= 1e-3

@@ -78,10 +78,10 @@ int main(int argc, char** argv) {
   {
     unsigned long long t[128];
     tzc_trace_dump(t);
-    printf("  tile 5 epilogue (thread 128): start=%lld bar1=%lld chunk0=%lld chunk1=%lld chunk2=%lld bar2=%lld tma=%lld end=%lld\n",
-           (long long)(t[18 + 5 * 5 - 5] - t[0]), (long long)(t[120] - t[0]), (long long)(t[121] - t[0]),
+    printf("  tile 4 epilogue (thread 128): start=%lld waitread=%lld bar1=%lld c0=%lld c1=%lld c2=%lld c3=%lld bar2=%lld tma=%lld end=%lld\n",
+           (long long)(t[13 + 5 * 4] - t[0]), (long long)(t[119] - t[0]), (long long)(t[120] - t[0]), (long long)(t[121] - t[0]),
            (long long)(t[122] - t[0]), (long long)(t[123] - t[0]), (long long)(t[124] - t[0]), (long long)(t[125] - t[0]),
-           (long long)(t[14 + 5 * 5] - t[0]));
+           (long long)(t[126] - t[0]), (long long)(t[14 + 5 * 4] - t[0]));
   }
   return 0;
 }
