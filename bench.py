@@ -52,6 +52,7 @@ def parse():
     ap.add_argument("--layers", default="", help="comma list of layer names (default: all 23)")
     ap.add_argument("--profile", default="i8", choices=["i8", "f16"],
                     help="i8: the BASELINE metric (default); f16: configs[3] (fp16 in, fp32 accumulate, fp16 out)")
+    ap.add_argument("--opt", action="append", default=[], help="name=value passed to tzc_b200_set_option (tuning)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-threads", type=int, default=3, help="host threads issuing run_op calls in the e2e leg")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -208,6 +209,9 @@ def run_ours(args, rank, world, local):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     assert lib().tzc_b200_device_ok() == 1, "libtzc_b200: no sm_100 device"
+    for o in args.opt:
+        k, v = o.split("=")
+        D.set_option(k, int(v))
     names = [s for s in args.layers.split(",") if s]
     gen = torch.Generator(device=dev)
     gen.manual_seed(1234 + rank)

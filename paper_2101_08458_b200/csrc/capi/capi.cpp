@@ -229,6 +229,10 @@ int tzc_b200_set_option(const char* name, int64_t value) {
     set_tail_split((int)value);
     return TZC_OK;
   }
+  if (n == "split_min_kb") {
+    set_split_min_kb((int)value);
+    return TZC_OK;
+  }
   if (n == "pingpong_kb") {
     set_pingpong_kb((int)value);
     return TZC_OK;

@@ -36,6 +36,12 @@ constexpr int kStaticSmem = 0;
 #endif
 // General-kernel SMEM: EG int8 staging tiles (128 x BN) + the A/B ring + barriers.
 int ring_smem(int bn, int kb, int eg, int stages) { return 1024 + eg * 128 * bn + stages * (128 + bn) * kb + 256; }
+// set_option "split_min_kb": automatic split-K for under-filled grids keeps
+// >= this many K blocks per split.  Off by default: in the multi-branch
+// graph step other layers' CTAs fill idle SMs, and the int32 partial round
+// trip + fix-up launch cost more (batch 32: 511 -> 572 TOPS without it,
+// batch 64: 660 -> 804).
+int g_split_min_kb = 1 << 20;
 int g_pingpong_kb = 2;  // set_option "pingpong_kb": max K blocks per tile for ping-pong epilogue groups
 int epi_groups_for(int kb_per_tile) { return kb_per_tile <= g_pingpong_kb ? 2 : 1; }
 
@@ -62,7 +68,7 @@ WorkSplit work_split(int tiles, int tiles_n, int num_kb, int sms, bool ok16, int
   if (tiles < sms) {
     // fill the machine, keeping >= 8 K blocks per split so the int32 partial
     // round trip stays small next to the MMA work
-    const int s = std::min((sms + tiles - 1) / tiles, num_kb / 8);
+    const int s = std::min((sms + tiles - 1) / tiles, num_kb / g_split_min_kb);
     if (s >= 2) {
       w.splits = s;
       w.full = 0;
@@ -308,6 +314,7 @@ void set_ws_enabled(int on) { g_ws_enabled = on; }
 void set_tma_store(int on) { g_tma_store = on; }
 void set_ws_1x1(int on) { g_ws_1x1 = on ? 1 : 0; }
 void set_pingpong_kb(int kb) { g_pingpong_kb = kb; }
+void set_split_min_kb(int kb) { g_split_min_kb = kb < 1 ? 1 : kb; }
 void set_ws_mt(int mt) { g_ws_mt = (mt == 1 || mt == 2 || mt == 4) ? mt : 0; }
 void set_forced_bn(int bn) { g_forced_bn = (bn == 64 || bn == 128 || bn == 256) ? bn : 0; }
 void set_ws_epi_groups(int g) { g_ws_epi_groups = g == 1 ? 1 : 2; }

@@ -47,6 +47,7 @@ void set_forced_bn(int bn);
 void set_ws_1x1(int on);
 void set_ws_mt(int mt);
 void set_pingpong_kb(int kb);
+void set_split_min_kb(int kb);
 void set_tail_split(int on);
 void set_ws_epi_groups(int g);
 int device_ok();
