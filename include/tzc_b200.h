@@ -149,11 +149,20 @@ TZC_API int tzc_b200_plan_conv(const tzc_conv_desc* d, tzc_plan* plan);
 TZC_API int tzc_b200_plan_gemm(const tzc_gemm_desc* d, tzc_plan* plan);
 /* Force a split-K factor for subsequent launches (0 = automatic). */
 TZC_API int tzc_b200_set_splits(int32_t splits);
-/* Process-wide options: "splits" (as above), "shifted_window" (1 = use the
- * weight-stationary shifted-window kernel for eligible stride-1 convs, the
- * default; 0 = always TMA im2col), "tma_store" (1 = int8 requant outputs are
- * staged in shared memory and written by TMA, the default; 0 = direct
- * per-thread stores). */
+/* Process-wide tuning options (all default to the measured-best setting;
+ * results never change, only the kernel plan):
+ *   "splits"         force a split-K factor (0 = automatic)
+ *   "split_min_kb"   automatic split-K when a grid underfills the GPU, keeping
+ *                    >= this many K blocks per split (default: off)
+ *   "tail_split"     split the under-filled last round of tiles (default 0)
+ *   "shifted_window" weight-stationary shifted-window kernel for eligible
+ *                    stride-1 convs (default 1; 0 = always TMA im2col)
+ *   "ws_1x1"         force the shifted-window kernel for every 1x1 stride-1 conv
+ *   "ws_mt"          force its 128-row tiles per work unit (1, 2, 4; 0 = auto)
+ *   "ws_epi_groups"  1 or 2 epilogue groups in the shifted-window kernel
+ *   "pingpong_kb"    ping-pong epilogue groups for tiles of <= this many K blocks
+ *   "bn"             force the N tile (64, 128, 256; 0 = automatic)
+ *   "tma_store"      int8 requant outputs staged in SMEM and written by TMA (1). */
 TZC_API int tzc_b200_set_option(const char* name, int64_t value);
 
 /* K5 layout adapter for the reference's channel-blocked conv2d_tdsl layouts
