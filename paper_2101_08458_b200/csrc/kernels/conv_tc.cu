@@ -285,6 +285,7 @@ struct Scratch {
 std::map<cudaStream_t, Scratch> g_ws;
 int g_ws_epi_groups = 1;  // shifted-window epilogue groups (set_option "ws_epi_groups")
 int g_tma_store = 1;   // TMA-store int8 epilogue (set_option "tma_store")
+int g_l2_hints = 1;    // set_option "l2_hints": 1 = A loads evict-first (default), 2 = B loads evict-last
 int g_forced_bn = 0;   // set_option "bn" (0 = automatic)
 int g_ws_mt = 0;       // set_option "ws_mt": force the shifted-window tiles per unit (0 = automatic)
 int g_ws_1x1 = 0;      // set_option "ws_1x1": force the weight-stationary kernel for every 1x1 stride-1 conv
@@ -312,6 +313,7 @@ void set_forced_splits(int s) { g_forced_splits = s; }
 void set_tail_split(int on) { g_tail_split = on ? 1 : 0; }
 void set_ws_enabled(int on) { g_ws_enabled = on; }
 void set_tma_store(int on) { g_tma_store = on; }
+void set_l2_hints(int h) { g_l2_hints = h & 3; }
 void set_ws_1x1(int on) { g_ws_1x1 = on ? 1 : 0; }
 void set_pingpong_kb(int kb) { g_pingpong_kb = kb; }
 void set_split_min_kb(int kb) { g_split_min_kb = kb < 1 ? 1 : kb; }
@@ -638,6 +640,8 @@ Status run_ws(const Problem& pb, const WsPlan& w, const void* a, const void* b, 
 #ifdef TZC_TRACE
   p.debug_flags = ::g_debug_flags;
 #endif
+  p.pol_a = (g_l2_hints & 1) ? tzcdev::kL2EvictFirst : 0;
+  p.pol_b = (g_l2_hints & 2) ? tzcdev::kL2EvictLast : 0;
   p.magic_hw = ((uint64_t(1) << 40) + (uint64_t)pb.hp * pb.wp - 1) / ((uint64_t)pb.hp * pb.wp);
   p.magic_wp = ((uint64_t(1) << 40) + (uint64_t)pb.wp - 1) / (uint64_t)pb.wp;
   p.a_box_bytes = box_bytes;
@@ -773,6 +777,8 @@ Status run_problem(const Problem& pb, const void* a, const void* b, const void* 
 #ifdef TZC_TRACE
   p.debug_flags = ::g_debug_flags;
 #endif
+  p.pol_a = (g_l2_hints & 1) ? tzcdev::kL2EvictFirst : 0;
+  p.pol_b = (g_l2_hints & 2) ? tzcdev::kL2EvictLast : 0;
   // ---- A operand
   if (pb.a_mode == tzcdev::A_TILED) {
     cuuint64_t dims[2] = {(cuuint64_t)pb.a_kdim, (cuuint64_t)pb.a_rows};

@@ -135,6 +135,7 @@ struct alignas(64) ConvKernelParams {
   int32_t epi_groups;          // general kernel: 1 or 2 (ping-pong) epilogue groups
   uint64_t magic_hw, magic_wp; // ceil(2^40 / (Hp*Wp)), ceil(2^40 / Wp): exact q / d for q < 2^22
   int32_t debug_flags;         // tools only: 1 = skip epilogue body, 2 = skip epilogue stores
+  uint64_t pol_a, pol_b;       // TMA L2 cache policies for A / B loads (0 = no hint)
   // shifted-window MMA table: per MMA of a channel block, the A start-address
   // delta and the B offset (16-byte units).  Kernel parameters live in the
   // constant bank, so the issuing warp reads them straight into uniform
@@ -542,14 +543,14 @@ __global__ void __launch_bounds__(EpiCfg<BN>::THREADS, 1) conv_tc_kernel(const _
             tma_load_im2col_4d(dA, &p.tmA, &full[stage], cb * KE, ow * p.stride, oh * p.stride, img,
                                (uint16_t)s, (uint16_t)r);
           } else {
-            tma_load_2d(dA, &p.tmA, &full[stage], kb * KE, m0);
+            tma_load_2d_p(dA, &p.tmA, &full[stage], kb * KE, m0, p.pol_a);
           }
           if constexpr (kBMN) {
 #pragma unroll
             for (int j = 0; j < BN / 64; ++j)
-              tma_load_2d(dB + j * (KE * 128), &p.tmB, &full[stage], n0 + 64 * j, kb * KE);
+              tma_load_2d_p(dB + j * (KE * 128), &p.tmB, &full[stage], n0 + 64 * j, kb * KE, p.pol_b);
           } else {
-            tma_load_3d(dB, &p.tmB, &full[stage], cb * KE, n0, tap);
+            tma_load_3d_p(dB, &p.tmB, &full[stage], cb * KE, n0, tap, p.pol_b);
           }
           if (++stage == STAGES) {
             stage = 0;

@@ -118,7 +118,7 @@ __global__ void __launch_bounds__(EpiCfg<BN>::THREADS, 1) conv_ws_kernel(const _
           mbar_expect_tx(&afull[slot], p.a_nbox * p.a_box_bytes);
           const int row0 = kPair ? q0 >> 3 : q0;  // pair mode: 8 pixels per 128-byte TMA row
           for (int b = 0; b < p.a_nbox; ++b)
-            tma_load_2d(dA + b * p.a_box_bytes, &p.tmA, &afull[slot], cb * KE, row0 + b * p.box_rows);
+            tma_load_2d_p(dA + b * p.a_box_bytes, &p.tmA, &afull[slot], cb * KE, row0 + b * p.box_rows, p.pol_a);
           if (++slot == a_slots) {
             slot = 0;
             phase ^= 1;

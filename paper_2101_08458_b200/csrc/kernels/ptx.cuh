@@ -84,6 +84,36 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const void* tmap, uint64_
       "l"(reinterpret_cast<uint64_t>(tmap)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
       : "memory");
 }
+// L2 cache-policy hints for TMA (createpolicy-encoded constants: evict-first
+// for streamed operands, evict-last for operands every CTA re-reads)
+constexpr uint64_t kL2EvictFirst = 0x12F0000000000000ull;
+constexpr uint64_t kL2EvictLast = 0x14F0000000000000ull;
+__device__ __forceinline__ void tma_load_2d_hint(void* dst, const void* tmap, uint64_t* bar, int c0, int c1,
+                                                 uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d_hint(void* dst, const void* tmap, uint64_t* bar, int c0, int c1,
+                                                 int c2, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d_p(void* dst, const void* tmap, uint64_t* bar, int c0, int c1,
+                                              uint64_t pol) {
+  if (pol) tma_load_2d_hint(dst, tmap, bar, c0, c1, pol);
+  else tma_load_2d(dst, tmap, bar, c0, c1);
+}
+__device__ __forceinline__ void tma_load_3d_p(void* dst, const void* tmap, uint64_t* bar, int c0, int c1, int c2,
+                                              uint64_t pol) {
+  if (pol) tma_load_3d_hint(dst, tmap, bar, c0, c1, c2, pol);
+  else tma_load_3d(dst, tmap, bar, c0, c1, c2);
+}
 // im2col: coordinates (c, w, h, n) of the first output pixel's base input
 // pixel; offsets (s, r) select the filter tap.
 // ---- TMA stores (shared -> global, bulk async-group of the issuing thread) --
