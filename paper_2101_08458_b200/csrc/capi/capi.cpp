@@ -249,6 +249,10 @@ int tzc_b200_set_option(const char* name, int64_t value) {
     set_forced_bn((int)value);
     return TZC_OK;
   }
+  if (n == "st256") {
+    set_st256((int)value);
+    return TZC_OK;
+  }
   if (n == "l2_hints") {
     set_l2_hints((int)value);
     return TZC_OK;

@@ -285,6 +285,7 @@ struct Scratch {
 std::map<cudaStream_t, Scratch> g_ws;
 int g_ws_epi_groups = 1;  // shifted-window epilogue groups (set_option "ws_epi_groups")
 int g_tma_store = 1;   // TMA-store int8 epilogue (set_option "tma_store")
+int g_st256 = 1;      // set_option "st256": 256-bit epilogue stores where aligned
 int g_l2_hints = 1;    // set_option "l2_hints": 1 = A loads evict-first (default), 2 = B loads evict-last
 int g_forced_bn = 0;   // set_option "bn" (0 = automatic)
 int g_ws_mt = 0;       // set_option "ws_mt": force the shifted-window tiles per unit (0 = automatic)
@@ -314,6 +315,7 @@ void set_tail_split(int on) { g_tail_split = on ? 1 : 0; }
 void set_ws_enabled(int on) { g_ws_enabled = on; }
 void set_tma_store(int on) { g_tma_store = on; }
 void set_l2_hints(int h) { g_l2_hints = h & 3; }
+void set_st256(int on) { g_st256 = on ? 1 : 0; }
 void set_ws_1x1(int on) { g_ws_1x1 = on ? 1 : 0; }
 void set_pingpong_kb(int kb) { g_pingpong_kb = kb; }
 void set_split_min_kb(int kb) { g_split_min_kb = kb < 1 ? 1 : kb; }
@@ -717,6 +719,7 @@ void fill_epilogue(ConvKernelParams* pp, const Problem& pb, const void* seed, vo
               pb.out.nb == pb.ngemm)
                  ? 1
                  : 0;
+  p.vec32 = (p.simple && g_st256 && pb.out.stride_m % 32 == 0 && reinterpret_cast<uintptr_t>(out) % 32 == 0) ? 1 : 0;
 }
 
 // ---- launch --------------------------------------------------------------------

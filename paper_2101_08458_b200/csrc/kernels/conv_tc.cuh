@@ -136,6 +136,7 @@ struct alignas(64) ConvKernelParams {
   uint64_t magic_hw, magic_wp; // ceil(2^40 / (Hp*Wp)), ceil(2^40 / Wp): exact q / d for q < 2^22
   int32_t debug_flags;         // tools only: 1 = skip epilogue body, 2 = skip epilogue stores
   uint64_t pol_a, pol_b;       // TMA L2 cache policies for A / B loads (0 = no hint)
+  int32_t vec32;               // simple path: output rows / base 32-byte aligned (256-bit stores)
   // shifted-window MMA table: per MMA of a channel block, the A start-address
   // delta and the B offset (16-byte units).  Kernel parameters live in the
   // constant bank, so the issuing warp reads them straight into uniform
@@ -198,6 +199,11 @@ __device__ __forceinline__ uint32_t requant_general(int32_t c, float s) {
 
 __device__ __forceinline__ void st_v4(void* p, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
   asm volatile("st.global.v4.b32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(a), "r"(b), "r"(c), "r"(d)
+               : "memory");
+}
+__device__ __forceinline__ void st_v8(void* p, const uint32_t* w) {  // 32-byte aligned
+  asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p), "r"(w[0]), "r"(w[1]), "r"(w[2]),
+               "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7])
                : "memory");
 }
 __device__ __forceinline__ uint4 ld_v4(const void* p) {
@@ -378,8 +384,26 @@ __device__ __forceinline__ void epi_simple(const ConvKernelParams& p, int m, int
   const int32_t negmask = -(int32_t)((1u << p.pow2_k) - 1u);
   const int32_t mul = (int32_t)(1u << (32 - p.pow2_k));
   int8_t* o = static_cast<int8_t*>(p.out) + (int64_t)m * p.out_stride_m + n;
+  if (CW == 32 && !stg && p.vec32 && n + 32 <= p.Ngemm) {
+    // one 256-bit store per row chunk: whole 32-byte sectors (no half-sector
+    // L2 writes) and half the store instructions
+    uint32_t w[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      uint32_t b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int32_t c = (int32_t)v[4 * q + i];
+        b[i] = (uint32_t)__mulhi((c >> 31) * negmask + c, mul);
+      }
+      w[q] = __byte_perm(__byte_perm(b[0], b[1], 0x0040), __byte_perm(b[2], b[3], 0x0040), 0x5410);
+    }
+    st_v8(o, w);
+    return;
+  }
 #pragma unroll
   for (int j = 0; j < CW / 16; ++j) {
+    if (n + 16 * j >= p.Ngemm) break;  // ragged N: pieces past the last column
     uint32_t b[16];
 #pragma unroll
     for (int i = 0; i < 16; ++i) {

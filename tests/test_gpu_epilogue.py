@@ -63,3 +63,37 @@ def test_tma_store_output_untouched_outside(cuda):
     got = big.cpu().numpy()
     assert np.array_equal(got[:m], Orc.requant_i8(Orc.matmul(a, b), 2.0 ** -12))
     assert (got[m:] == 77).all()
+
+
+@pytest.mark.parametrize("n", [48, 80, 208, 96])
+@pytest.mark.parametrize("st256", [1, 0])
+def test_simple_requant_ragged_n_strided(cuda, n, st256):
+    """The 2^-k fast path (256-bit or 128-bit row stores) with N not a multiple
+    of the tile: columns past N inside a wider row buffer keep their bytes."""
+    m, k = 700, 64
+    a = Orc.random_tensor("u8", (m, k), 440)
+    b = Orc.random_tensor("i8", (n, k), 441)
+    big = torch.full((m, n + 112), 77, dtype=torch.int8, device=cuda)
+    D.set_option("st256", st256)
+    try:
+        D.gemm(to_dev(a, cuda), to_dev(b, cuda), epilogue="requant_i8", scale=2.0 ** -9, out=big,
+               out_layout=D.OutLayout(nb=n, stride_m=n + 112, stride_blk=0))
+    finally:
+        D.set_option("st256", 1)
+    got = big.cpu().numpy()
+    assert np.array_equal(got[:, :n], Orc.requant_i8(Orc.matmul(a, b), 2.0 ** -9))
+    assert (got[:, n:] == 77).all()
+
+
+@pytest.mark.parametrize("st256", [1, 0])
+def test_simple_requant_ws_conv_256bit(cuda, st256):
+    """Shifted-window conv (stride 1, 3x3) through the 256-bit store path."""
+    x = Orc.random_tensor("u8", (2, 20, 20, 64), 450)
+    w = Orc.random_tensor("i8", (64, 3, 3, 64), 451)
+    want = Orc.requant_i8(Orc.conv2d_nhwc(x, w, 1), 2.0 ** -12)
+    D.set_option("st256", st256)
+    try:
+        got = D.conv2d(to_dev(x, cuda), to_dev(w, cuda), 1, epilogue="requant_i8", scale=2.0 ** -12).cpu().numpy()
+    finally:
+        D.set_option("st256", 1)
+    assert np.array_equal(got, want)
