@@ -164,7 +164,11 @@ TZC_API int tzc_b200_set_splits(int32_t splits);
  *   "bn"             force the N tile (64, 128, 256; 0 = automatic)
  *   "tma_store"      int8 requant outputs staged in SMEM and written by TMA (1)
  *   "l2_hints"       TMA load L2 policies: bit 0 = activations evict-first
- *                    (default 1), bit 1 = weights evict-last. */
+ *                    (default 1), bit 1 = weights evict-last
+ *   "st256"          256-bit epilogue stores on the 2^-k requant path (1)
+ *   "pair"           CTA-pair kernel (tcgen05 cta_group::2, 256-row tiles, B
+ *                    split across the pair) for eligible int8 requant layers
+ *                    with >= 3 K blocks (default 0: measured no faster). */
 TZC_API int tzc_b200_set_option(const char* name, int64_t value);
 
 /* K5 layout adapter for the reference's channel-blocked conv2d_tdsl layouts

@@ -249,6 +249,10 @@ int tzc_b200_set_option(const char* name, int64_t value) {
     set_forced_bn((int)value);
     return TZC_OK;
   }
+  if (n == "pair") {
+    set_pair((int)value);
+    return TZC_OK;
+  }
   if (n == "st256") {
     set_st256((int)value);
     return TZC_OK;

@@ -22,6 +22,7 @@
 
 #include "../tzc_b200_internal.hpp"
 #include "conv_tc.cuh"
+#include "conv_tc2.cuh"
 #include "conv_ws.cuh"
 
 #ifdef TZC_TRACE
@@ -198,6 +199,47 @@ Status launch_kernel(const ConvKernelParams& p, int grid, cudaStream_t stream) {
   return Status();
 }
 
+// CTA-pair kernel (conv_tc2.cuh): clusters of 2 along x, PDL as above.
+int pair_smem(int bn, int stages) { return 1024 + 128 * bn + stages * (128 + bn / 2) * 128 + 256; }
+int pair_stages(int bn) { return std::min(8, (227 * 1024 - kStaticSmem - 1024 - 256 - 128 * bn) / ((128 + bn / 2) * 128)); }
+
+template <int BN, int AM>
+Status launch_pair(const ConvKernelParams& p, int grid, cudaStream_t stream) {
+  auto kern = tzcdev::conv_tc2_kernel<BN, AM>;
+  static bool attr_done = false;
+  if (!attr_done) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024 - kStaticSmem);
+    if (e != cudaSuccess) return Status(TZC_E_DEVICE, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
+    attr_done = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(tzcdev::EpiCfg<BN>::THREADS);
+  cfg.dynamicSmemBytes = pair_smem(BN, p.stages);
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  attr[1].id = cudaLaunchAttributeClusterDimension;
+  attr[1].val.clusterDim.x = 2;
+  attr[1].val.clusterDim.y = 1;
+  attr[1].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, p);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  if (e == cudaSuccess) e = cudaGetLastError();
+  if (e != cudaSuccess) return Status(TZC_E_DEVICE, std::string("conv_tc2 launch: ") + cudaGetErrorString(e));
+  return Status();
+}
+
+Status launch_pair_any(const ConvKernelParams& p, int bn, int am, int grid, cudaStream_t stream) {
+  if (bn == 256) return am == tzcdev::A_IM2COL ? launch_pair<256, tzcdev::A_IM2COL>(p, grid, stream)
+                                               : launch_pair<256, tzcdev::A_TILED>(p, grid, stream);
+  return am == tzcdev::A_IM2COL ? launch_pair<128, tzcdev::A_IM2COL>(p, grid, stream)
+                                : launch_pair<128, tzcdev::A_TILED>(p, grid, stream);
+}
+
 template <bool F16, int EPM>
 Status launch_reduce(const ConvKernelParams& p, cudaStream_t stream) {
   int64_t groups = (int64_t)p.red_rows * (p.Ngemm / 16);
@@ -285,6 +327,7 @@ struct Scratch {
 std::map<cudaStream_t, Scratch> g_ws;
 int g_ws_epi_groups = 1;  // shifted-window epilogue groups (set_option "ws_epi_groups")
 int g_tma_store = 1;   // TMA-store int8 epilogue (set_option "tma_store")
+int g_pair = 0;       // set_option "pair": CTA-pair (cta_group::2) kernel for eligible int8 layers
 int g_st256 = 1;      // set_option "st256": 256-bit epilogue stores where aligned
 int g_l2_hints = 1;    // set_option "l2_hints": 1 = A loads evict-first (default), 2 = B loads evict-last
 int g_forced_bn = 0;   // set_option "bn" (0 = automatic)
@@ -316,6 +359,7 @@ void set_ws_enabled(int on) { g_ws_enabled = on; }
 void set_tma_store(int on) { g_tma_store = on; }
 void set_l2_hints(int h) { g_l2_hints = h & 3; }
 void set_st256(int on) { g_st256 = on ? 1 : 0; }
+void set_pair(int on) { g_pair = on ? 1 : 0; }
 void set_ws_1x1(int on) { g_ws_1x1 = on ? 1 : 0; }
 void set_pingpong_kb(int kb) { g_pingpong_kb = kb; }
 void set_split_min_kb(int kb) { g_split_min_kb = kb < 1 ? 1 : kb; }
@@ -876,6 +920,29 @@ Status run_problem(const Problem& pb, const void* a, const void* b, const void* 
                    "cuTensorMapEncodeTiled(out)");
     if (!st.ok()) return st;
     p.tma_store = 1;
+  }
+  if (g_pair && p.tma_store && !pb.f16 && !pb.b_kn && plan.splits == 1 && p.full_units == p.num_tiles &&
+      p.epi_groups == 1 && plan.bk_bytes == 128 && (plan.bn == 128 || plan.bn == 256) &&
+      (pb.a_mode == tzcdev::A_TILED || pb.a_mode == tzcdev::A_IM2COL) && num_sms() >= 2) {
+    // CTA pairs: 256-row tiles, each CTA loads its A rows and half the B rows
+    const int64_t sk = pb.w_stride_k;
+    const int64_t stap = pb.taps > 1 ? pb.w_stride_tap : sk * pb.ngemm;
+    cuuint64_t dims[3] = {(cuuint64_t)pb.c, (cuuint64_t)pb.ngemm, (cuuint64_t)pb.taps};
+    cuuint64_t strides[2] = {(cuuint64_t)sk, (cuuint64_t)stap};
+    cuuint32_t box[3] = {(cuuint32_t)KE, (cuuint32_t)(plan.bn / 2), 1};
+    cuuint32_t es[3] = {1, 1, 1};
+    st = enc_check(p_encode_tiled(&p.tmB, dt, 3, const_cast<void*>(b), dims, strides, box, es,
+                                  CU_TENSOR_MAP_INTERLEAVE_NONE, swz(plan.bk_bytes),
+                                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE),
+                   "cuTensorMapEncodeTiled(B half)");
+    if (!st.ok()) return st;
+    const int pairs_m = (plan.tiles_m + 1) / 2;
+    p.num_tiles = pairs_m * plan.tiles_n;
+    p.full_units = p.num_tiles;
+    p.stages = pair_stages(plan.bn);
+    const int sms = num_sms() & ~1;
+    const int grid = (int)std::min<int64_t>(sms, 2 * (int64_t)p.num_tiles);
+    return launch_pair_any(p, plan.bn, pb.a_mode, grid, stream);
   }
   if (plan.splits > 1) {
     st = workspace(0, (size_t)plan.workspace_bytes, &p.partial, stream);
