@@ -162,7 +162,9 @@ TZC_API int tzc_b200_set_splits(int32_t splits);
  *   "ws_epi_groups"  1 or 2 epilogue groups in the shifted-window kernel
  *   "pingpong_kb"    ping-pong epilogue groups for tiles of <= this many K blocks
  *   "bn"             force the N tile (64, 128, 256; 0 = automatic)
- *   "tma_store"      int8 requant outputs staged in SMEM and written by TMA (1)
+ *   "tma_store"      int8 requant outputs staged in SMEM and written by TMA:
+ *                    0 never (default), 1 always, 2 when the GEMM K is at
+ *                    most "tma_store_k" bytes (default 64)
  *   "l2_hints"       TMA load L2 policies: bit 0 = activations evict-first
  *                    (default 1), bit 1 = weights evict-last
  *   "st256"          256-bit epilogue stores on the 2^-k requant path (1)

@@ -249,6 +249,10 @@ int tzc_b200_set_option(const char* name, int64_t value) {
     set_forced_bn((int)value);
     return TZC_OK;
   }
+  if (n == "tma_store_k") {
+    set_tma_store_k((int)value);
+    return TZC_OK;
+  }
   if (n == "pair") {
     set_pair((int)value);
     return TZC_OK;
@@ -262,7 +266,7 @@ int tzc_b200_set_option(const char* name, int64_t value) {
     return TZC_OK;
   }
   if (n == "tma_store") {
-    set_tma_store(value ? 1 : 0);
+    set_tma_store((int)value);
     return TZC_OK;
   }
   return report(Status(TZC_E_VALIDATION, "unknown option '" + n + "'"));

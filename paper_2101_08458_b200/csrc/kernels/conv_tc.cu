@@ -326,7 +326,13 @@ struct Scratch {
 };
 std::map<cudaStream_t, Scratch> g_ws;
 int g_ws_epi_groups = 1;  // shifted-window epilogue groups (set_option "ws_epi_groups")
-int g_tma_store = 1;   // TMA-store int8 epilogue (set_option "tma_store")
+// TMA-store int8 epilogue (set_option "tma_store": 0 never, 1 always, 2 = GEMM
+// K of at most g_tma_store_k bytes).  Since the direct epilogue writes whole
+// 32-byte sectors with 256-bit row stores it wins in the multi-branch suite
+// (b256: always 1273, K <= 64 only 1324, never 1333 TOPS), although the
+// K = 64 layer alone is faster with TMA stores (c2_1x1_64_256 96 -> 89 us).
+int g_tma_store = 0;
+int g_tma_store_k = 64;
 int g_pair = 0;       // set_option "pair": CTA-pair (cta_group::2) kernel for eligible int8 layers
 int g_st256 = 1;      // set_option "st256": 256-bit epilogue stores where aligned
 int g_l2_hints = 1;    // set_option "l2_hints": 1 = A loads evict-first (default), 2 = B loads evict-last
@@ -356,7 +362,8 @@ Status workspace(int slot, size_t bytes, void** out, cudaStream_t stream) {
 void set_forced_splits(int s) { g_forced_splits = s; }
 void set_tail_split(int on) { g_tail_split = on ? 1 : 0; }
 void set_ws_enabled(int on) { g_ws_enabled = on; }
-void set_tma_store(int on) { g_tma_store = on; }
+void set_tma_store(int on) { g_tma_store = on < 0 ? 0 : (on > 2 ? 2 : on); }
+void set_tma_store_k(int k) { g_tma_store_k = k; }
 void set_l2_hints(int h) { g_l2_hints = h & 3; }
 void set_st256(int on) { g_st256 = on ? 1 : 0; }
 void set_pair(int on) { g_pair = on ? 1 : 0; }
@@ -906,7 +913,8 @@ Status run_problem(const Problem& pb, const void* a, const void* b, const void* 
   p.fd_s = make_fdiv(std::max(1, pb.s));
   fill_epilogue(&p, pb, seed, out, ep);
   if (ep.kind == tzcdev::EP_REQUANT_I8 && p.full_units > 0 && p.vec_ok && pb.out.nb == pb.ngemm &&
-      pb.out.stride_m == pb.ngemm && pb.ngemm % plan.bn == 0 && g_tma_store) {
+      pb.out.stride_m == pb.ngemm && pb.ngemm % plan.bn == 0 &&
+      (g_tma_store == 1 || (g_tma_store == 2 && (int64_t)p.num_kb * plan.bk_bytes <= g_tma_store_k))) {
     // int8 output as a [M, Ngemm] map; one box = 32 rows x min(BN, 128) bytes
     const int rb = std::min(plan.bn, 128);
     cuuint64_t dims[2] = {(cuuint64_t)pb.ngemm, (cuuint64_t)pb.m};

@@ -43,6 +43,7 @@ Status run_problem(const Problem& pb, const void* a, const void* b, const void* 
 void set_forced_splits(int s);
 void set_ws_enabled(int on);
 void set_tma_store(int on);
+void set_tma_store_k(int k);
 void set_l2_hints(int h);
 void set_st256(int on);
 void set_pair(int on);

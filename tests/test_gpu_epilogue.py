@@ -20,7 +20,7 @@ def gemm_q(cuda, a, b, scale, seed=None, tma=True):
         return D.gemm(to_dev(a, cuda), to_dev(b, cuda), None if seed is None else to_dev(seed, cuda),
                       epilogue="requant_i8", scale=scale).cpu().numpy()
     finally:
-        D.set_option("tma_store", 1)
+        D.set_option("tma_store", 0)
 
 
 @pytest.mark.parametrize("m,n,k", [(1000, 64, 64), (777, 128, 128), (1283, 256, 64), (300, 512, 256),
@@ -49,8 +49,13 @@ def test_tma_store_conv_requant(cuda, n, hp, c, k, r, stride):
     w = Orc.random_tensor("i8", (k, r, r, c), 421)
     scale = 2.0 ** -13
     want = Orc.requant_i8(Orc.conv2d_nhwc(x, w, stride), scale)
-    got = D.conv2d(to_dev(x, cuda), to_dev(w, cuda), stride, epilogue="requant_i8", scale=scale).cpu().numpy()
-    assert np.array_equal(got, want)
+    for tma in (1, 0):
+        D.set_option("tma_store", tma)
+        try:
+            got = D.conv2d(to_dev(x, cuda), to_dev(w, cuda), stride, epilogue="requant_i8", scale=scale).cpu().numpy()
+        finally:
+            D.set_option("tma_store", 0)
+        assert np.array_equal(got, want), tma
 
 
 def test_tma_store_output_untouched_outside(cuda):
@@ -58,11 +63,16 @@ def test_tma_store_output_untouched_outside(cuda):
     m, n, k = 1000, 256, 64
     a = Orc.random_tensor("u8", (m, k), 430)
     b = Orc.random_tensor("i8", (n, k), 431)
-    big = torch.full((m + 200, n), 77, dtype=torch.int8, device=cuda)
-    D.gemm(to_dev(a, cuda), to_dev(b, cuda), epilogue="requant_i8", scale=2.0 ** -12, out=big[:m])
-    got = big.cpu().numpy()
-    assert np.array_equal(got[:m], Orc.requant_i8(Orc.matmul(a, b), 2.0 ** -12))
-    assert (got[m:] == 77).all()
+    for tma in (1, 0):
+        big = torch.full((m + 200, n), 77, dtype=torch.int8, device=cuda)
+        D.set_option("tma_store", tma)
+        try:
+            D.gemm(to_dev(a, cuda), to_dev(b, cuda), epilogue="requant_i8", scale=2.0 ** -12, out=big[:m])
+        finally:
+            D.set_option("tma_store", 0)
+        got = big.cpu().numpy()
+        assert np.array_equal(got[:m], Orc.requant_i8(Orc.matmul(a, b), 2.0 ** -12))
+        assert (got[m:] == 77).all()
 
 
 @pytest.mark.parametrize("n", [48, 80, 208, 96])

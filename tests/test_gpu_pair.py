@@ -15,11 +15,14 @@ PAIR_DEFAULT = 0  # the library default (conv_tc.cu g_pair)
 
 
 def with_pair(on, fn):
+    """The pair kernel runs the TMA-store epilogue: force it for every tile."""
     D.set_option("pair", on)
+    D.set_option("tma_store", 1)
     try:
         return fn()
     finally:
         D.set_option("pair", PAIR_DEFAULT)
+        D.set_option("tma_store", 0)
 
 
 @pytest.mark.parametrize("m,n,k", [(1000, 256, 512), (777, 128, 384), (4096, 256, 1024), (300, 512, 256 + 128),

@@ -100,7 +100,7 @@ def test_ws_requant_tiny_images(cuda, n, hp, c, k, r):
             try:
                 got = run(cuda, x, w, 1, seed, epilogue="requant_i8", scale=scale)
             finally:
-                D.set_option("tma_store", 1)
+                D.set_option("tma_store", 0)
             assert np.array_equal(got, want), (scale, tma)
 
 
