@@ -170,7 +170,7 @@ TZC_API int tzc_b200_set_splits(int32_t splits);
  *   "st256"          256-bit epilogue stores on the 2^-k requant path (1)
  *   "pair"           CTA-pair kernel (tcgen05 cta_group::2, 256-row tiles, B
  *                    split across the pair) for eligible int8 requant layers
- *                    with >= 3 K blocks (default 0: measured no faster). */
+ *                    (default 0) with >= "pair_min_kb" K blocks (default 16) */
 TZC_API int tzc_b200_set_option(const char* name, int64_t value);
 
 /* K5 layout adapter for the reference's channel-blocked conv2d_tdsl layouts

@@ -253,6 +253,10 @@ int tzc_b200_set_option(const char* name, int64_t value) {
     set_tma_store_k((int)value);
     return TZC_OK;
   }
+  if (n == "pair_min_kb") {
+    set_pair_min_kb((int)value);
+    return TZC_OK;
+  }
   if (n == "pair") {
     set_pair((int)value);
     return TZC_OK;

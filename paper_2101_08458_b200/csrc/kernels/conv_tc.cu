@@ -333,7 +333,16 @@ int g_ws_epi_groups = 1;  // shifted-window epilogue groups (set_option "ws_epi_
 // K = 64 layer alone is faster with TMA stores (c2_1x1_64_256 96 -> 89 us).
 int g_tma_store = 0;
 int g_tma_store_k = 64;
-int g_pair = 0;       // set_option "pair": CTA-pair (cta_group::2) kernel for eligible int8 layers
+// set_option "pair": CTA-pair (cta_group::2) kernel for eligible int8 layers
+// with >= g_pair_min_kb K blocks ("pair_min_kb").  It wins on the deep-K
+// layers (3x3 at 14x14 / 7x7: 2-3 us each) and loses on K <= 1 KiB ones,
+// where the pair's coupled pipelines (one MMA issuer, both epilogues on the
+// leader's barrier) cost more than the halved B stream saves.  Off by
+// default: in the multi-branch suite the per-layer gains do not carry over
+// (b256 1325 -> 1315 TOPS, b32 654 -> 637): a cluster needs two free SMs of
+// one TPC, so pair CTAs fill the SMs other branches leave idle less well.
+int g_pair = 0;
+int g_pair_min_kb = 16;
 int g_st256 = 1;      // set_option "st256": 256-bit epilogue stores where aligned
 int g_l2_hints = 1;    // set_option "l2_hints": 1 = A loads evict-first (default), 2 = B loads evict-last
 int g_forced_bn = 0;   // set_option "bn" (0 = automatic)
@@ -367,6 +376,7 @@ void set_tma_store_k(int k) { g_tma_store_k = k; }
 void set_l2_hints(int h) { g_l2_hints = h & 3; }
 void set_st256(int on) { g_st256 = on ? 1 : 0; }
 void set_pair(int on) { g_pair = on ? 1 : 0; }
+void set_pair_min_kb(int kb) { g_pair_min_kb = kb; }
 void set_ws_1x1(int on) { g_ws_1x1 = on ? 1 : 0; }
 void set_pingpong_kb(int kb) { g_pingpong_kb = kb; }
 void set_split_min_kb(int kb) { g_split_min_kb = kb < 1 ? 1 : kb; }
@@ -929,7 +939,8 @@ Status run_problem(const Problem& pb, const void* a, const void* b, const void* 
     if (!st.ok()) return st;
     p.tma_store = 1;
   }
-  if (g_pair && p.tma_store && !pb.f16 && !pb.b_kn && plan.splits == 1 && p.full_units == p.num_tiles &&
+  if (g_pair && ep.kind == tzcdev::EP_REQUANT_I8 && p.vec_ok && pb.ngemm % plan.bn == 0 && !pb.f16 && !pb.b_kn &&
+      plan.splits == 1 && p.full_units == p.num_tiles && p.num_kb >= g_pair_min_kb &&
       p.epi_groups == 1 && plan.bk_bytes == 128 && (plan.bn == 128 || plan.bn == 256) &&
       (pb.a_mode == tzcdev::A_TILED || pb.a_mode == tzcdev::A_IM2COL) && num_sms() >= 2) {
     // CTA pairs: 256-row tiles, each CTA loads its A rows and half the B rows

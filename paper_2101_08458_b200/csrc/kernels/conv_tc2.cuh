@@ -1,13 +1,14 @@
 // conv_tc2_kernel: the general tiled / TMA-im2col conv-GEMM on CTA pairs
-// (cta_group::2), for the int8 requant + TMA-store epilogue.
+// (cta_group::2), for the int8 requant epilogue (direct or TMA-store).
 //
-// Why: the deep ResNet layers are bound by the L2 -> SMEM operand stream
-// (~6300 B/cycle chip-wide), not by the tensor pipe.  A single-CTA 128 x BN
-// tile pulls 128 + BN operand rows per K block; a pair computes one 256 x BN
+// Why: a single-CTA 128 x BN tile pulls 128 + BN operand rows per K block
+// through L2 -> SMEM (~6300 B/cycle chip-wide); a pair computes one 256 x BN
 // tile with ONE M=256 MMA stream, each CTA holding its 128 A rows and HALF
 // of the B rows (the MMA reads B[0, BN/2) from CTA 0 and B[BN/2, BN) from
 // CTA 1), so a CTA pulls 128 + BN/2 rows: -33 % L2 -> SMEM bytes at BN=256,
-// -25 % at BN=128.
+// -25 % at BN=128.  Measured: 2-3 us faster per deep-K layer (3x3 at 14x14
+// and 7x7), slower on K <= 1 KiB layers, and no gain in the multi-branch
+// suite, so it is opt-in (set_option "pair").
 //
 // Roles (both CTAs run all of them except the MMA issuer):
 //   warp 0   TMA producer: waits its own `empty` slot, loads its A / B half,
@@ -176,20 +177,29 @@ __global__ void __launch_bounds__(EpiCfg<BN>::THREADS, 1) conv_tc2_kernel(const 
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const uint32_t tq = tmem_base + ((q * 32) << 16) + acc * BN;
-      if (h == 0 && lane == 0) bulk_wait_read0();  // the previous store has read the staging
-      named_bar_sync(bar, 128);
+      if (p.tma_store) {
+        if (h == 0 && lane == 0) bulk_wait_read0();  // the previous store has read the staging
+        named_bar_sync(bar, 128);
 #pragma unroll 1
-      for (int c = 0; c < HALF / CW; ++c) {
-        const int col = h * HALF + c * CW;
-        epi_chunk<CW, false, EPM_REQUANT, BN>(p, tq + col, m < p.M ? m : -1, n_tile * BN + col, true, smem_u32(stq),
-                                              (int)lane, col);
-      }
-      fence_proxy_async_smem();
-      named_bar_sync(bar, 128);
-      if (h == 0 && lane == 0 && m_tile * BM < p.M) {
+        for (int c = 0; c < HALF / CW; ++c) {
+          const int col = h * HALF + c * CW;
+          epi_chunk<CW, false, EPM_REQUANT, BN>(p, tq + col, m < p.M ? m : -1, n_tile * BN + col, true,
+                                                smem_u32(stq), (int)lane, col);
+        }
+        fence_proxy_async_smem();
+        named_bar_sync(bar, 128);
+        if (h == 0 && lane == 0 && m_tile * BM < p.M) {
 #pragma unroll
-        for (int b = 0; b < BN / RB; ++b) tma_store_2d(&p.tmO, stq + b * (32 * RB), n_tile * BN + b * RB, m_tile * BM + q * 32);
-        bulk_commit();
+          for (int b = 0; b < BN / RB; ++b)
+            tma_store_2d(&p.tmO, stq + b * (32 * RB), n_tile * BN + b * RB, m_tile * BM + q * 32);
+          bulk_commit();
+        }
+      } else {  // direct row stores (whole N tile in range: host-checked)
+#pragma unroll 1
+        for (int c = 0; c < HALF / CW; ++c) {
+          const int col = h * HALF + c * CW;
+          epi_chunk<CW, false, EPM_REQUANT, BN>(p, tq + col, m < p.M ? m : -1, n_tile * BN + col, true);
+        }
       }
       tc_fence_before();
       __syncwarp();
@@ -199,7 +209,7 @@ __global__ void __launch_bounds__(EpiCfg<BN>::THREADS, 1) conv_tc2_kernel(const 
         acc_phase ^= 1;
       }
     }
-    if (h == 0 && lane == 0) bulk_wait0();
+    if (p.tma_store && h == 0 && lane == 0) bulk_wait0();
   }
   __syncwarp();
   __syncthreads();

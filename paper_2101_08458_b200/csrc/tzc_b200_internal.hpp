@@ -47,6 +47,7 @@ void set_tma_store_k(int k);
 void set_l2_hints(int h);
 void set_st256(int on);
 void set_pair(int on);
+void set_pair_min_kb(int kb);
 void set_forced_bn(int bn);
 void set_ws_1x1(int on);
 void set_ws_mt(int mt);

@@ -11,17 +11,20 @@ from paper_2101_08458_b200 import device as D
 from tests.gpu_helpers import to_dev
 
 pytestmark = pytest.mark.gpu
-PAIR_DEFAULT = 0  # the library default (conv_tc.cu g_pair)
+PAIR_DEFAULT = 0  # the library defaults (conv_tc.cu g_pair, g_pair_min_kb)
+PAIR_MIN_KB = 16
 
 
 def with_pair(on, fn):
     """The pair kernel runs the TMA-store epilogue: force it for every tile."""
     D.set_option("pair", on)
+    D.set_option("pair_min_kb", 1)
     D.set_option("tma_store", 1)
     try:
         return fn()
     finally:
         D.set_option("pair", PAIR_DEFAULT)
+        D.set_option("pair_min_kb", PAIR_MIN_KB)
         D.set_option("tma_store", 0)
 
 
@@ -55,4 +58,20 @@ def test_pair_general_requant_scale(cuda):
     want = Orc.requant_i8(Orc.matmul(a, b), 0.00037)
     got = with_pair(1, lambda: D.gemm(to_dev(a, cuda), to_dev(b, cuda), epilogue="requant_i8",
                                       scale=0.00037).cpu().numpy())
+    assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("m,n,k", [(1000, 256, 512), (129, 128, 640)])
+def test_pair_direct_store_epilogue(cuda, m, n, k):
+    """The pair kernel with the direct (256-bit row store) epilogue."""
+    a = Orc.random_tensor("u8", (m, k), 530)
+    b = Orc.random_tensor("i8", (n, k), 531)
+    want = Orc.requant_i8(Orc.matmul(a, b), 2.0 ** -12)
+    D.set_option("pair", 1)
+    D.set_option("pair_min_kb", 1)
+    try:
+        got = D.gemm(to_dev(a, cuda), to_dev(b, cuda), epilogue="requant_i8", scale=2.0 ** -12).cpu().numpy()
+    finally:
+        D.set_option("pair", PAIR_DEFAULT)
+        D.set_option("pair_min_kb", PAIR_MIN_KB)
     assert np.array_equal(got, want)
