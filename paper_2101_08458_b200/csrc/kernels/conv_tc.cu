@@ -781,6 +781,14 @@ void fill_epilogue(ConvKernelParams* pp, const Problem& pb, const void* seed, vo
                  ? 1
                  : 0;
   p.vec32 = (p.simple && g_st256 && pb.out.stride_m % 32 == 0 && reinterpret_cast<uintptr_t>(out) % 32 == 0) ? 1 : 0;
+  {
+    const int eo = (ep.kind == tzcdev::EP_REQUANT_I8) ? 1 : (ep.kind == tzcdev::EP_CAST_F16) ? 2 : 4;
+    auto al32 = [eo](int64_t elems) { return (elems * eo) % 32 == 0; };
+    p.st32 = (g_st256 && eo > 1 && p.vec_ok && al32(pb.out.stride_m) && al32(pb.out.stride_blk) && al32(pb.out.nb) &&
+              reinterpret_cast<uintptr_t>(out) % 32 == 0)
+                 ? 1
+                 : 0;
+  }
 }
 
 // ---- launch --------------------------------------------------------------------

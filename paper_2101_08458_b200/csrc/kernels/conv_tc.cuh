@@ -137,6 +137,7 @@ struct alignas(64) ConvKernelParams {
   int32_t debug_flags;         // tools only: 1 = skip epilogue body, 2 = skip epilogue stores
   uint64_t pol_a, pol_b;       // TMA L2 cache policies for A / B loads (0 = no hint)
   int32_t vec32;               // simple path: output rows / base 32-byte aligned (256-bit stores)
+  int32_t st32;                // vector path, f16 / 32-bit outputs: every 16-column piece 32-byte aligned
   // shifted-window MMA table: per MMA of a channel block, the A start-address
   // delta and the B offset (16-byte units).  Kernel parameters live in the
   // constant bank, so the issuing warp reads them straight into uniform
@@ -338,8 +339,12 @@ __device__ __forceinline__ void store16(const ConvKernelParams& p, int m, int n,
     }
     if constexpr (vec) {
       uint16_t* o = static_cast<uint16_t*>(p.out) + off;
-      st_v4(o, w[0], w[1], w[2], w[3]);
-      st_v4(o + 8, w[4], w[5], w[6], w[7]);
+      if (p.st32) {
+        st_v8(o, w);  // 16 halves = one 32-byte sector
+      } else {
+        st_v4(o, w[0], w[1], w[2], w[3]);
+        st_v4(o + 8, w[4], w[5], w[6], w[7]);
+      }
     } else {
 #pragma unroll
       for (int i = 0; i < 16; ++i)
@@ -348,8 +353,13 @@ __device__ __forceinline__ void store16(const ConvKernelParams& p, int m, int n,
   } else {  // raw 32-bit accumulator image (i32 / f32)
     if constexpr (vec) {
       uint32_t* o = static_cast<uint32_t*>(p.out) + off;
+      if (p.st32) {
+        st_v8(o, a);
+        st_v8(o + 8, a + 8);
+      } else {
 #pragma unroll
-      for (int j = 0; j < 4; ++j) st_v4(o + 4 * j, a[4 * j], a[4 * j + 1], a[4 * j + 2], a[4 * j + 3]);
+        for (int j = 0; j < 4; ++j) st_v4(o + 4 * j, a[4 * j], a[4 * j + 1], a[4 * j + 2], a[4 * j + 3]);
+      }
     } else {
 #pragma unroll
       for (int i = 0; i < 16; ++i)

@@ -107,3 +107,23 @@ def test_simple_requant_ws_conv_256bit(cuda, st256):
     finally:
         D.set_option("st256", 1)
     assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("st256", [1, 0])
+def test_wide_stores_f16_and_raw_outputs(cuda, st256):
+    """fp16-cast and raw int32 outputs through the 256-bit (st256=1) and the
+    128-bit store paths: identical bytes."""
+    from tests.gpu_helpers import rel_dev
+    x = Orc.random_tensor("fp16", (2, 12, 12, 64), 460)
+    w = Orc.random_tensor("fp16", (128, 3, 3, 64), 461)
+    a = Orc.random_tensor("u8", (300, 256), 462)
+    b = Orc.random_tensor("i8", (192, 256), 463)
+    D.set_option("st256", st256)
+    try:
+        h = D.conv2d(to_dev(x, cuda, True), to_dev(w, cuda, True), 1, epilogue="f16").cpu()
+        i32 = D.gemm(to_dev(a, cuda), to_dev(b, cuda)).cpu().numpy()
+    finally:
+        D.set_option("st256", 1)
+    hv = h.view(torch.int16).numpy().view(np.uint16).view(np.float16).astype(np.float64)
+    assert rel_dev(Orc.conv2d_nhwc(x, w, 1, fp16=True), hv) <= 1e-3 + 2 ** -11
+    assert np.array_equal(i32, Orc.matmul(a, b))
