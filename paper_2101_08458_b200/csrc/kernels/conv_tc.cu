@@ -191,7 +191,7 @@ Status launch_kernel(const ConvKernelParams& p, int grid, cudaStream_t stream) {
     if (e != cudaSuccess) return Status(TZC_E_DEVICE, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
     attr_done = true;
   }
-  const int smem = ring_smem(BN, KB, p.epi_groups, p.stages);
+  const int smem = ring_smem(BN, KB, p.tma_store ? p.epi_groups : 0, p.stages);  // staging only for TMA stores
   cudaError_t e = launch_pdl(kern, dim3(grid), dim3(tzcdev::EpiCfg<BN>::THREADS), smem, stream, p);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   if (e == cudaSuccess) e = cudaGetLastError();
@@ -947,6 +947,8 @@ Status run_problem(const Problem& pb, const void* a, const void* b, const void* 
     if (!st.ok()) return st;
     p.tma_store = 1;
   }
+  // without the TMA-store staging tiles the ring gets their SMEM
+  if (!p.tma_store) p.stages = ring_stages(plan.bn, plan.bk_bytes, 0);
   if (g_pair && ep.kind == tzcdev::EP_REQUANT_I8 && p.vec_ok && pb.ngemm % plan.bn == 0 && !pb.f16 && !pb.b_kn &&
       plan.splits == 1 && p.full_units == p.num_tiles && p.num_kb >= g_pair_min_kb &&
       p.epi_groups == 1 && plan.bk_bytes == 128 && (plan.bn == 128 || plan.bn == 256) &&

@@ -508,7 +508,7 @@ __global__ void __launch_bounds__(EpiCfg<BN>::THREADS, 1) conv_tc_kernel(const _
   TZC_TRACE_INIT;
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sStage = smem;  // TMA-store staging: EG tiles of STAGING_BYTES (1024-aligned)
-  uint8_t* sA = smem + EG * Cfg::STAGING_BYTES;
+  uint8_t* sA = smem + (p.tma_store ? EG * Cfg::STAGING_BYTES : 0);
   uint8_t* sB = sA + STAGES * Cfg::A_BYTES;
   uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * Cfg::B_BYTES);
   uint64_t* empty = full + STAGES;
