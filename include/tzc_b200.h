@@ -158,6 +158,8 @@ TZC_API int tzc_b200_set_splits(int32_t splits);
  *   "shifted_window" weight-stationary shifted-window kernel for eligible
  *                    stride-1 convs (default 1; 0 = always TMA im2col)
  *   "ws_1x1"         force the shifted-window kernel for every 1x1 stride-1 conv
+ *   "ws_1x1_k"       ... and use it for 1x1 stride-1 convs with K <= this many
+ *                    bytes (default 64)
  *   "ws_mt"          force its 128-row tiles per work unit (1, 2, 4; 0 = auto)
  *   "ws_epi_groups"  1 or 2 epilogue groups in the shifted-window kernel
  *   "pingpong_kb"    ping-pong epilogue groups for tiles of <= this many K blocks

@@ -241,6 +241,10 @@ int tzc_b200_set_option(const char* name, int64_t value) {
     set_ws_mt((int)value);
     return TZC_OK;
   }
+  if (n == "ws_1x1_k") {
+    set_ws_1x1_k((int)value);
+    return TZC_OK;
+  }
   if (n == "ws_1x1") {
     set_ws_1x1((int)value);
     return TZC_OK;

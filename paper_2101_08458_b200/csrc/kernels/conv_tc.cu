@@ -348,6 +348,7 @@ int g_l2_hints = 1;    // set_option "l2_hints": 1 = A loads evict-first (defaul
 int g_forced_bn = 0;   // set_option "bn" (0 = automatic)
 int g_ws_mt = 0;       // set_option "ws_mt": force the shifted-window tiles per unit (0 = automatic)
 int g_ws_1x1 = 0;      // set_option "ws_1x1": force the weight-stationary kernel for every 1x1 stride-1 conv
+int g_ws_1x1_k = 64;   // set_option "ws_1x1_k": ... and for 1x1 convs with K <= this many bytes
 int g_forced_splits = 0;
 int g_ws_enabled = 1;  // shifted-window kernel for eligible stride-1 convs (TZC_B200_NO_WS=1 disables)
 
@@ -378,6 +379,7 @@ void set_st256(int on) { g_st256 = on ? 1 : 0; }
 void set_pair(int on) { g_pair = on ? 1 : 0; }
 void set_pair_min_kb(int kb) { g_pair_min_kb = kb; }
 void set_ws_1x1(int on) { g_ws_1x1 = on ? 1 : 0; }
+void set_ws_1x1_k(int k) { g_ws_1x1_k = k; }
 void set_pingpong_kb(int kb) { g_pingpong_kb = kb; }
 void set_split_min_kb(int kb) { g_split_min_kb = kb < 1 ? 1 : kb; }
 void set_ws_mt(int mt) { g_ws_mt = (mt == 1 || mt == 2 || mt == 4) ? mt : 0; }
@@ -576,7 +578,11 @@ bool ws_plan(const Problem& pb, bool pair, WsPlan* w) {
   // 1x1: weight-stationary pays off only for a single 64-wide N tile and one
   // K block (c2_1x1_64_64: 43 -> 31 us at batch 256); wider layers keep the
   // TMA-store general kernel (measured, tools/layer_timing.py --opt ws_1x1=1)
-  if (pb.taps < 2 && !g_ws_1x1 && !(pb.ngemm == 64 && (int64_t)pb.c * (pb.f16 ? 2 : 1) <= 128)) return false;
+  // With the direct 256-bit-store epilogue the single-K-block 1x1 layers of
+  // any width gain too (c2_1x1_64_256: 96 -> 76 us): "ws_1x1_k" bytes of K.
+  if (pb.taps < 2 && !g_ws_1x1 && !(pb.ngemm == 64 && (int64_t)pb.c * (pb.f16 ? 2 : 1) <= 128) &&
+      !((int64_t)pb.c * (pb.f16 ? 2 : 1) <= g_ws_1x1_k))
+    return false;
   if (!(pb.ngemm == 64 || pb.ngemm == 128 || pb.ngemm == 256)) return false;
   const int e = pb.f16 ? 2 : 1;
   const int64_t cb = (int64_t)pb.c * e;

@@ -50,6 +50,7 @@ void set_pair(int on);
 void set_pair_min_kb(int kb);
 void set_forced_bn(int bn);
 void set_ws_1x1(int on);
+void set_ws_1x1_k(int k);
 void set_ws_mt(int mt);
 void set_pingpong_kb(int kb);
 void set_split_min_kb(int kb);
