@@ -22,12 +22,15 @@
 //                                              inspect; + fused dp groups (F6)
 //   rewriter.hpp (tile_and_reorder)            tile_and_reorder -> TensorizedOp with a
 //                                              device KernelPlan (tiles, TMA layouts)
-//   vm.hpp (TensorValue, random_inputs,        same value types; eval_tir's role is
-//           compare, eval_tir)                 taken by run_tensorized (device)
+//   rewriter.hpp (Schedule, lower,              same; Pad is realised in-kernel (TMA OOB)
+//     inject_intrinsic) / tensor_ir.hpp        print_tensor_ir = the reference's snapshot text
+//   vm.hpp (TensorValue, random_inputs,        same value types; eval_tir runs tcgen05 nests
+//           compare, eval_tir)                 on the B200 (run_tensorized), nothing on a CPU VM
 #ifndef TZC_B200_TZC_HPP
 #define TZC_B200_TZC_HPP
 
 #include <cstdint>
+#include <functional>
 #include <map>
 #include <memory>
 #include <optional>
@@ -295,6 +298,85 @@ TensorizedOp tile_and_reorder(const ComputeOp& op, const Intrinsic& intr, const 
 // Convenience: match, pick the first device-realisable mapping, tile.
 TensorizedOp tensorize(const ComputeOp& op, const Intrinsic& intr);
 
+// ============================ schedules + tensor IR ======================
+// The reference's lowering chain (proj/include/tzc/rewriter.hpp:14-116,
+// proj/include/tzc/tensor_ir.hpp:13-78): a Schedule applied to an op gives
+// the imperative TensorIR nest; inject_intrinsic replaces its tensorize
+// pragma nest with one instruction call; eval_tir executes it — here on the
+// B200 only (tcgen05 descriptions), never on a CPU interpreter.
+struct Transform {
+  enum class Kind : uint8_t { Pad, Split, Reorder, Fuse, Parallel, Unroll, SplitReduction, Pragma };
+  Kind kind = Kind::Split;
+  std::string a, b;
+  std::vector<std::string> names;
+  int64_t factor = 0;
+  static std::string kind_name(Kind k);
+};
+using Schedule = std::vector<Transform>;
+std::string print_schedule(const Schedule& s);     // one transform per line
+Schedule parse_schedule(const std::string& text);  // SyntaxError on bad lines
+Schedule load_schedule(const std::string& path);   // IoError when unreadable
+
+enum class LoopAnn : uint8_t { Serial, Parallel, Unrolled, Tensorize };
+std::string loop_ann_name(LoopAnn a);
+
+struct Stmt;
+using StmtPtr = std::shared_ptr<const Stmt>;
+struct Stmt {
+  enum class Kind : uint8_t { For, Store, Intrinsic, Seq };
+  Kind kind = Kind::Seq;
+  std::string var;  // For
+  int64_t extent = 0;
+  LoopAnn ann = LoopAnn::Serial;
+  StmtPtr body;
+  std::string tensor;             // Store / Intrinsic destination
+  std::vector<ExprPtr> indices;   // Store
+  ExprPtr value;                  // Store
+  std::string intrinsic;          // Intrinsic
+  ExprPtr dst_index;              // Intrinsic: lane scatter pattern
+  std::vector<ExprPtr> args;      // Intrinsic: one vector operand per input register
+  std::vector<StmtPtr> stmts;     // Seq
+};
+StmtPtr make_for(std::string var, int64_t extent, StmtPtr body, LoopAnn ann = LoopAnn::Serial);
+StmtPtr make_store(std::string tensor, std::vector<ExprPtr> indices, ExprPtr value);
+StmtPtr make_intrinsic(std::string name, std::string dst_tensor, ExprPtr dst_index, std::vector<ExprPtr> args);
+StmtPtr make_seq(std::vector<StmtPtr> stmts);
+
+struct TensorIR {
+  std::vector<TensorDecl> tensors;
+  std::vector<std::string> temps;
+  std::string output;
+  bool seed_output = false;
+  StmtPtr root;
+  std::vector<Intrinsic> intrinsics;
+  // Backend extension: the op the nest was lowered from and the mapping the
+  // injected call realises; eval_tir turns them into the device KernelPlan.
+  std::shared_ptr<const ComputeOp> source;
+  LoopMapping mapping;
+  const TensorDecl* find_tensor(const std::string& name) const;
+  const Intrinsic* find_intrinsic(const std::string& name) const;
+};
+std::string print_tensor_ir(const TensorIR& ir);  // the reference's golden-snapshot format
+void visit_stmts(const StmtPtr& s, const std::function<void(const Stmt&)>& f);
+int count_stmts(const StmtPtr& s, Stmt::Kind kind);
+
+struct LinearSplit {
+  ExprPtr residual;  // never null
+  std::map<std::string, int64_t> coeff;
+};
+std::optional<LinearSplit> split_linear(const ExprPtr& e, const std::vector<std::string>& vars);
+
+struct LowerOptions {
+  bool literal_unroll = false;
+};
+// Pad transforms throw PadUnsupported: this backend realises padding with
+// TMA out-of-bounds zero fill inside the kernel (tile_and_reorder's plan).
+TensorIR lower(const ComputeOp& op, const Schedule& schedule, const LowerOptions& opts = {});
+TensorIR lower(const ComputeOp& op, const std::vector<std::string>& schedule_lines, const LowerOptions& opts = {});
+TensorIR inject_intrinsic(const TensorIR& ir, const Intrinsic& intr, const LoopMapping& mapping);
+// lower(tile_and_reorder schedule) + inject for the first device-realisable mapping.
+TensorIR tensorized_ir(const ComputeOp& op, const Intrinsic& intr);
+
 // ============================ values =====================================
 struct TensorValue {
   DType dtype;
@@ -321,6 +403,14 @@ Deviation compare(const TensorValue& ref, const TensorValue& got, double rtol);
 // `epilogue_op` (optional) is the reference-expressible requantize / cast
 // op over the output, fused into the kernel.
 TensorValue run_tensorized(const TensorizedOp& t, const Inputs& inputs, const ComputeOp* epilogue_op = nullptr);
+
+// The reference's eval_tir (proj/include/tzc/vm.hpp:50, src/vm.cpp:510-516):
+// executes an injected TensorIR.  Only nests whose single call is a tcgen05
+// description run (on the B200); anything else throws InjectError — there is
+// no CPU interpreter behind this entry point.
+TensorValue eval_tir(const TensorIR& ir, const Inputs& inputs, const ComputeOp* epilogue_op = nullptr);
+// The device plan eval_tir executes for `ir` (InjectError as above).
+TensorizedOp device_plan(const TensorIR& ir);
 
 // Packed-buffer form used by the C ABI (tzc_b200_run_op): buffers at the
 // declared element width, row-major.

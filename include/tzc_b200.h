@@ -197,7 +197,22 @@ TZC_API int tzc_b200_run_op(const char* op_tdsl, const char* intrinsic, const ch
                     int32_t n_inputs, const char* const* names, const void* const* host_inputs,
                     void* host_out, int64_t out_bytes);
 
+/* The reference's lowering chain, `lower` -> `inject_intrinsic` -> `eval_tir`
+ * (proj/include/tzc/rewriter.hpp:85-95, vm.hpp:50; driven the same way by
+ * `tzc verify`, proj/src/cli.cpp:227-283).  `schedule` is schedule text
+ * (proj/src/rewriter.cpp:30-131 grammar) or NULL for tile_and_reorder's
+ * schedule of the first device-realisable mapping.  The nest must hold one
+ * tcgen05 call; other instructions return TZC_E_INJECT (no CPU VM).  Buffers
+ * as for tzc_b200_run_op. */
+TZC_API int tzc_b200_eval_tir(const char* op_tdsl, const char* schedule, const char* intrinsic,
+                              const char* requant_tdsl, int32_t n_inputs, const char* const* names,
+                              const void* const* host_inputs, void* host_out, int64_t out_bytes);
+
 /* ---- host-library introspection (op text in, text out; no GPU needed) --------- */
+/* print_tensor_ir(lower(op, schedule)), injected with `intrinsic` when it is
+ * non-NULL (schedule NULL: the tensorized IR of the first device mapping):
+ * the reference's golden-snapshot text (proj/src/tensor_ir.cpp print format). */
+TZC_API int tzc_b200_lower(const char* op_tdsl, const char* schedule, const char* intrinsic, char* buf, int64_t buflen);
 /* parse_compute + infer_types + print_compute (proj/src/compute_op.cpp:285-313). */
 TZC_API int tzc_b200_parse(const char* op_tdsl, char* buf, int64_t buflen);
 /* inspect(): one "<mapping>" line per feasible mapping, in the reference's

@@ -97,6 +97,7 @@ class Ref:
                                               C.POINTER(_P), _P, _I64]
                 L.tzcref_tensorize.argtypes = [C.c_char_p, C.c_char_p, C.c_char_p, _I64]
                 L.tzcref_inspect.argtypes = [C.c_char_p, C.c_char_p, C.c_char_p, _I64]
+                L.tzcref_lower.argtypes = [C.c_char_p, C.c_char_p, C.c_char_p, C.c_char_p, _I64]
                 L.tzcref_matmul_tdsl.argtypes = [_I64, _I64, _I64, C.c_int, C.c_char_p, _I64]
                 L.tzcref_conv2d_tdsl.argtypes = [_I64] * 7 + [C.c_int, C.c_char_p, _I64]
                 L.tzcref_f64_to_f16_bits.argtypes = [C.c_double]
@@ -134,6 +135,11 @@ class Ref:
     @classmethod
     def tensorize(cls, op_text, intrinsic) -> str:
         return cls._text(cls.lib().tzcref_tensorize, op_text.encode(), intrinsic.encode())
+
+    @classmethod
+    def lower(cls, op_text, schedule, intrinsic=None) -> str:
+        return cls._text(cls.lib().tzcref_lower, op_text.encode(), schedule.encode(),
+                         None if intrinsic is None else intrinsic.encode())
 
     @classmethod
     def inspect(cls, op_text, intrinsic) -> list:

@@ -215,6 +215,18 @@ int tzcref_tensorize(const char* op_text, const char* intrinsic, char* buf,
   TZCREF_CATCH
 }
 
+// print_tensor_ir(lower(op, parse_schedule(schedule))), injected with
+// `intrinsic` when non-NULL (empty mapping: inject only checks its size).
+int tzcref_lower(const char* op_text, const char* schedule, const char* intrinsic,
+                 char* buf, int64_t buflen) {
+  TZCREF_TRY
+  ComputeOp op = op_from(op_text);
+  TensorIR ir = lower(op, parse_schedule(schedule));
+  if (intrinsic) ir = inject_intrinsic(ir, resolve_intrinsic(intrinsic), LoopMapping{});
+  return put_text(print_tensor_ir(ir), buf, buflen);
+  TZCREF_CATCH
+}
+
 // "<assignment> <needs_padding>\n" per mapping; empty when no match.
 int tzcref_inspect(const char* op_text, const char* intrinsic, char* buf,
                    int64_t buflen) {

@@ -135,3 +135,46 @@ extern "C" TZC_API int tzc_b200_builtins(char* buf, int64_t n) {
 extern "C" TZC_API int tzc_b200_print_intrinsic(const char* intrinsic, char* buf, int64_t n) {
   return guarded([&] { return put(tzc::print_intrinsic(tzc::resolve_intrinsic(intrinsic)), buf, n); });
 }
+
+// ---- the reference's lowering chain (lower -> inject_intrinsic -> eval_tir) ----
+namespace {
+
+tzc::TensorIR lowered(const char* op_tdsl, const char* schedule, const char* intrinsic) {
+  const tzc::ComputeOp op = tzc::infer_types(tzc::parse_compute(op_tdsl));
+  if (!schedule) {
+    if (!intrinsic) throw tzc::MissingInput("NULL schedule needs an intrinsic");
+    return tzc::tensorized_ir(op, tzc::resolve_intrinsic(intrinsic));
+  }
+  tzc::TensorIR ir = tzc::lower(op, tzc::parse_schedule(schedule));
+  if (intrinsic) ir = tzc::inject_intrinsic(ir, tzc::resolve_intrinsic(intrinsic), tzc::LoopMapping{});
+  return ir;
+}
+
+}  // namespace
+
+extern "C" TZC_API int tzc_b200_lower(const char* op_tdsl, const char* schedule, const char* intrinsic, char* buf,
+                                      int64_t n) {
+  return guarded([&] {
+    if (!op_tdsl) throw tzc::MissingInput("NULL op");
+    return put(tzc::print_tensor_ir(lowered(op_tdsl, schedule, intrinsic)), buf, n);
+  });
+}
+
+extern "C" TZC_API int tzc_b200_eval_tir(const char* op_tdsl, const char* schedule, const char* intrinsic,
+                                         const char* requant_tdsl, int32_t n_inputs, const char* const* names,
+                                         const void* const* host_inputs, void* host_out, int64_t out_bytes) {
+  return guarded([&] {
+    if (!op_tdsl || !intrinsic || !host_out || (n_inputs > 0 && (!names || !host_inputs)))
+      throw tzc::MissingInput("NULL argument");
+    const tzc::TensorizedOp t = tzc::device_plan(lowered(op_tdsl, schedule, intrinsic));
+    std::map<std::string, const void*> in;
+    for (int32_t i = 0; i < n_inputs; ++i) in[names[i]] = host_inputs[i];
+    if (requant_tdsl) {
+      const tzc::ComputeOp ep = tzc::parse_compute(requant_tdsl);
+      tzc::run_tensorized_packed(t, in, host_out, out_bytes, &ep);
+    } else {
+      tzc::run_tensorized_packed(t, in, host_out, out_bytes, nullptr);
+    }
+    return TZC_OK;
+  });
+}

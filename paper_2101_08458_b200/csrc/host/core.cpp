@@ -110,8 +110,16 @@ ExprPtr load(const std::string& tensor, std::vector<ExprPtr> idx, DType t) {
   return e;
 }
 ExprPtr cast(DType t, ExprPtr s) { return make(Expr::Kind::Cast, t, {std::move(s)}); }
-ExprPtr add(ExprPtr a, ExprPtr b) { return make(Expr::Kind::Add, DType(), {std::move(a), std::move(b)}); }
-ExprPtr mul(ExprPtr a, ExprPtr b) { return make(Expr::Kind::Mul, DType(), {std::move(a), std::move(b)}); }
+// Binary nodes take the left operand's type (untyped until infer_types for
+// parsed ops; typed when lowering builds `out + term` from typed parts).
+ExprPtr add(ExprPtr a, ExprPtr b) {
+  const DType t = a->dtype;
+  return make(Expr::Kind::Add, t, {std::move(a), std::move(b)});
+}
+ExprPtr mul(ExprPtr a, ExprPtr b) {
+  const DType t = a->dtype;
+  return make(Expr::Kind::Mul, t, {std::move(a), std::move(b)});
+}
 ExprPtr floordiv(ExprPtr a, ExprPtr b) { return make(Expr::Kind::FloorDiv, kI32, {std::move(a), std::move(b)}); }
 ExprPtr floormod(ExprPtr a, ExprPtr b) { return make(Expr::Kind::FloorMod, kI32, {std::move(a), std::move(b)}); }
 ExprPtr ramp(ExprPtr base, int64_t stride, int64_t lanes) {
@@ -121,7 +129,8 @@ ExprPtr ramp(ExprPtr base, int64_t stride, int64_t lanes) {
   return e;
 }
 ExprPtr broadcast(ExprPtr v, int64_t lanes) {
-  auto e = std::const_pointer_cast<Expr>(make(Expr::Kind::Broadcast, v->dtype, {std::move(v)}));
+  const DType t = v->dtype;  // read before the move below (argument order is unspecified)
+  auto e = std::const_pointer_cast<Expr>(make(Expr::Kind::Broadcast, t, {std::move(v)}));
   e->lanes_arg = lanes;
   return e;
 }
@@ -222,7 +231,18 @@ std::string float_text(double v) {
   if (s.find_first_of(".eEn") == std::string::npos) s += ".0";
   return s;
 }
-int prec(const ExprPtr& e) { return e->kind == Expr::Kind::Add ? 1 : e->kind == Expr::Kind::Mul ? 2 : 3; }
+int prec(const ExprPtr& e) {
+  switch (e->kind) {
+    case Expr::Kind::Add:
+      return 1;
+    case Expr::Kind::Mul:
+    case Expr::Kind::FloorDiv:
+    case Expr::Kind::FloorMod:
+      return 2;
+    default:
+      return 3;
+  }
+}
 }  // namespace
 
 std::string expr_to_string(const ExprPtr& e) {
@@ -251,9 +271,9 @@ std::string expr_to_string(const ExprPtr& e) {
     case Expr::Kind::Mul:
       return wrap(e->args[0], 2) + " * " + wrap(e->args[1], 3);
     case Expr::Kind::FloorDiv:
-      return "floordiv(" + list(e->args) + ")";
+      return wrap(e->args[0], 2) + " / " + wrap(e->args[1], 3);  // reference spelling (src/expr.cpp:342-347)
     case Expr::Kind::FloorMod:
-      return "floormod(" + list(e->args) + ")";
+      return wrap(e->args[0], 2) + " % " + wrap(e->args[1], 3);
     case Expr::Kind::Ramp:
       return "ramp(" + expr_to_string(e->args[0]) + ", " + std::to_string(e->ival) + ", " + std::to_string(e->lanes_arg) + ")";
     case Expr::Kind::Broadcast:

@@ -62,7 +62,26 @@ def declarations(op_text: str):
     return out
 
 
-def run_op(op_text: str, intrinsic: str, inputs: dict, epilogue: str | None = None, out: np.ndarray | None = None):
+def _enc(s):
+    return None if s is None else s.encode()
+
+
+def lower(op_text: str, schedule: str | None = None, intrinsic: str | None = None) -> str:
+    """print_tensor_ir(lower(op, schedule)) (+ inject_intrinsic when ``intrinsic``
+    is given); ``schedule=None`` uses tile_and_reorder's schedule of the first
+    device-realisable mapping (proj/include/tzc/rewriter.hpp:85-95)."""
+    return _text(lib().tzc_b200_lower, op_text.encode(), _enc(schedule), _enc(intrinsic))
+
+
+def eval_tir(op_text: str, intrinsic: str, inputs: dict, schedule: str | None = None, epilogue: str | None = None,
+             out: np.ndarray | None = None):
+    """The reference chain lower -> inject_intrinsic -> eval_tir, executed on the
+    B200 (tcgen05 instructions only).  Buffers as for :func:`run_op`."""
+    return run_op(op_text, intrinsic, inputs, epilogue, out, _schedule=schedule, _via_ir=True)
+
+
+def run_op(op_text: str, intrinsic: str, inputs: dict, epilogue: str | None = None, out: np.ndarray | None = None,
+           _schedule: str | None = None, _via_ir: bool = False):
     """Execute the tensorized op on the GPU from host buffers.
 
     ``inputs`` maps tensor names to arrays at the declared element width
@@ -80,8 +99,11 @@ def run_op(op_text: str, intrinsic: str, inputs: dict, epilogue: str | None = No
     arrs = [np.ascontiguousarray(inputs[n]) for n in names]
     cn = (C.c_char_p * len(names))(*[n.encode() for n in names])
     cp = (C.c_void_p * len(names))(*[a.ctypes.data for a in arrs])
-    rc = lib().tzc_b200_run_op(op_text.encode(), intrinsic.encode(),
-                               None if epilogue is None else epilogue.encode(), len(names), cn, cp,
-                               C.c_void_p(out.ctypes.data), out.nbytes)
+    if _via_ir:
+        rc = lib().tzc_b200_eval_tir(op_text.encode(), _enc(_schedule), intrinsic.encode(), _enc(epilogue),
+                                     len(names), cn, cp, C.c_void_p(out.ctypes.data), out.nbytes)
+    else:
+        rc = lib().tzc_b200_run_op(op_text.encode(), intrinsic.encode(), _enc(epilogue), len(names), cn, cp,
+                                   C.c_void_p(out.ctypes.data), out.nbytes)
     check(rc)
     return out

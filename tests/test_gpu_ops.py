@@ -112,3 +112,38 @@ def test_run_op_concurrent_threads(cuda):
     for (text, ins, ref), outs in zip(cases, results):
         for got in outs:
             assert np.array_equal(got, ref)
+
+
+# ---- the reference chain lower -> inject_intrinsic -> eval_tir on the device ----
+MM_SCHED = "split x 128\nsplit y {n}\nsplit k 32\nreorder x.o y.o k.o x.i y.i k.i\npragma x.i y.i k.i\n"
+
+
+@pytest.mark.parametrize("n", [64, 256])
+def test_eval_tir_matmul_reference_schedule(cuda, n):
+    """An explicit reference-grammar schedule, injected with tcgen05 and executed
+    by eval_tir: bit-exact vs the oracle, with and without the fused requant."""
+    text = matmul_tdsl(256, 512, 192)
+    ins = Orc.random_inputs(decls(text), 31)
+    ref = Orc.matmul(ins["A"], ins["B"], ins["C"])
+    intr = f"tcgen05_i8_m128n{n}k32"
+    assert np.array_equal(ops.eval_tir(text, intr, ins, schedule=MM_SCHED.format(n=n)), ref)
+    q = ops.eval_tir(text, intr, ins, schedule=MM_SCHED.format(n=n), epilogue=requant_tdsl((256, 512), 2.0 ** -13))
+    assert np.array_equal(q, Orc.requant_i8(ref, 2.0 ** -13))
+
+
+def test_eval_tir_conv_fused_pixel_group(cuda):
+    """The tile_and_reorder schedule (fused n.oh.ow onto M), lowered, injected, run."""
+    text = conv2d_nhwc_tdsl(2, 12, 12, 64, 128, 3, 3, 1)
+    ins = Orc.random_inputs(decls(text), 8)
+    ref = Orc.conv2d_nhwc(ins["data"], ins["kernel"], 1, ins["out"])
+    assert np.array_equal(ops.eval_tir(text, "tcgen05_i8_m128n64k32", ins), ref)
+
+
+def test_eval_tir_blocked_c1_matches_reference_sha(cuda):
+    """configs[0] exactly as the reference lowers it, through eval_tir: the
+    sha256 of the reference's own output (tests/golden/c1.npz)."""
+    g = np.load(os.path.join(GOLD, "c1.npz"))
+    text = str(g["text"])
+    ins = Orc.random_inputs(decls(text), int(g["seed"]))
+    out = ops.eval_tir(text, "tcgen05_i8_m128n64k32", ins)
+    assert hashlib.sha256(out.tobytes()).hexdigest() == str(g["sha_i32"])
