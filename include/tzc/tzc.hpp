@@ -31,6 +31,7 @@
 
 #include <cstdint>
 #include <functional>
+#include <iosfwd>
 #include <map>
 #include <memory>
 #include <optional>
@@ -396,6 +397,17 @@ struct Deviation {
   bool bitexact = true;
 };
 Deviation compare(const TensorValue& ref, const TensorValue& got, double rtol);
+
+// The reference's tensor container (proj/include/tzc/vm.hpp:108-116,
+// proj/src/vm.cpp:686-822): "TNSR", version u8 = 1, dtype code u8
+// (u8 i8 u16 i16 u32 i32 fp16 fp32 = 0..7), rank u8, little-endian u64
+// extents, raw little-endian elements at the declared width.  IoError on
+// malformed input.
+void write_tensor(std::ostream& os, const TensorValue& v);
+TensorValue read_tensor(std::istream& is);
+void save_tensor(const std::string& path, const TensorValue& v);
+TensorValue load_tensor(const std::string& path);
+std::string tensor_to_text(const TensorValue& v, int64_t max_elems = 64);
 
 // Executes a tensorized op on the B200 (the role eval_tir plays on the
 // reference VM).  Inputs as for eval_tir: declared inputs plus, for

@@ -221,6 +221,10 @@ TZC_API int tzc_b200_parse(const char* op_tdsl, char* buf, int64_t buflen);
 TZC_API int tzc_b200_inspect(const char* op_tdsl, const char* intrinsic, int32_t grouped, char* buf, int64_t buflen);
 /* tensorize(): chosen mapping, reference schedule text and the kernel plan. */
 TZC_API int tzc_b200_describe(const char* op_tdsl, const char* intrinsic, char* buf, int64_t buflen);
+/* The reference's TNSR tensor container (proj/src/vm.cpp:686-822):
+ * tensor_to_text(load_tensor(path), max_elems), and load + save (a format check). */
+TZC_API int tzc_b200_tensor_text(const char* path, int64_t max_elems, char* buf, int64_t buflen);
+TZC_API int tzc_b200_tensor_roundtrip(const char* src_path, const char* dst_path);
 /* builtin_names(), one per line. */
 TZC_API int tzc_b200_builtins(char* buf, int64_t buflen);
 /* print_intrinsic(resolve_intrinsic(ref)): the .intr text (proj/src/intrinsics.cpp:298-314). */

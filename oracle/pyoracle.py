@@ -98,6 +98,8 @@ class Ref:
                 L.tzcref_tensorize.argtypes = [C.c_char_p, C.c_char_p, C.c_char_p, _I64]
                 L.tzcref_inspect.argtypes = [C.c_char_p, C.c_char_p, C.c_char_p, _I64]
                 L.tzcref_lower.argtypes = [C.c_char_p, C.c_char_p, C.c_char_p, C.c_char_p, _I64]
+                L.tzcref_save_case.argtypes = [C.c_char_p, C.c_uint64, C.c_char_p]
+                L.tzcref_tensor_text.argtypes = [C.c_char_p, _I64, C.c_char_p, _I64]
                 L.tzcref_matmul_tdsl.argtypes = [_I64, _I64, _I64, C.c_int, C.c_char_p, _I64]
                 L.tzcref_conv2d_tdsl.argtypes = [_I64] * 7 + [C.c_int, C.c_char_p, _I64]
                 L.tzcref_f64_to_f16_bits.argtypes = [C.c_double]
@@ -135,6 +137,14 @@ class Ref:
     @classmethod
     def tensorize(cls, op_text, intrinsic) -> str:
         return cls._text(cls.lib().tzcref_tensorize, op_text.encode(), intrinsic.encode())
+
+    @classmethod
+    def save_case(cls, op_text, seed, directory):
+        cls._check(cls.lib().tzcref_save_case(op_text.encode(), seed, directory.encode()))
+
+    @classmethod
+    def tensor_text(cls, path, max_elems=1 << 30) -> str:
+        return cls._text(cls.lib().tzcref_tensor_text, path.encode(), max_elems, cap=1 << 26)
 
     @classmethod
     def lower(cls, op_text, schedule, intrinsic=None) -> str:

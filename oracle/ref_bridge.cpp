@@ -227,6 +227,26 @@ int tzcref_lower(const char* op_text, const char* schedule, const char* intrinsi
   TZCREF_CATCH
 }
 
+// Writes random_inputs(op, seed) (the tensors an eval needs) as
+// <dir>/<name>.tnsr and eval_reference's output as <dir>/expect.tnsr, with
+// the reference's own save_tensor: fixtures for the device CLI's verify.
+int tzcref_save_case(const char* op_text, uint64_t seed, const char* dir) {
+  TZCREF_TRY
+  ComputeOp op = op_from(op_text);
+  Inputs in = random_inputs(op, seed);
+  for (const auto& [name, v] : in) save_tensor(std::string(dir) + "/" + name + ".tnsr", v);
+  save_tensor(std::string(dir) + "/expect.tnsr", eval_reference(op, in));
+  return 0;
+  TZCREF_CATCH
+}
+
+// tensor_to_text(load_tensor(path), max_elems) as the reference renders it.
+int tzcref_tensor_text(const char* path, int64_t max_elems, char* buf, int64_t buflen) {
+  TZCREF_TRY
+  return put_text(tensor_to_text(load_tensor(path), max_elems), buf, buflen);
+  TZCREF_CATCH
+}
+
 // "<assignment> <needs_padding>\n" per mapping; empty when no match.
 int tzcref_inspect(const char* op_text, const char* intrinsic, char* buf,
                    int64_t buflen) {

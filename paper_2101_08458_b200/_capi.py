@@ -28,6 +28,7 @@ EXPORTS = (
     "tzc_b200_conv2d_i8", "tzc_b200_conv2d_f16", "tzc_b200_gemm_i8", "tzc_b200_gemm_f16",
     "tzc_b200_plan_conv", "tzc_b200_plan_gemm", "tzc_b200_set_splits", "tzc_b200_set_option",
     "tzc_b200_unblock_data", "tzc_b200_unblock_kernel", "tzc_b200_run_op", "tzc_b200_eval_tir", "tzc_b200_lower",
+    "tzc_b200_tensor_text", "tzc_b200_tensor_roundtrip",
     "tzc_b200_parse", "tzc_b200_inspect", "tzc_b200_describe", "tzc_b200_builtins",
     "tzc_b200_print_intrinsic",
     "tzc_b200_last_error", "tzc_b200_launch_count", "tzc_b200_device_ok", "tzc_b200_version",
@@ -105,6 +106,8 @@ def lib():
             L.tzc_b200_eval_tir.argtypes = [C.c_char_p, C.c_char_p, C.c_char_p, C.c_char_p, C.c_int32,
                                             C.POINTER(C.c_char_p), C.POINTER(P), P, C.c_int64]
             L.tzc_b200_lower.argtypes = [C.c_char_p, C.c_char_p, C.c_char_p, C.c_char_p, C.c_int64]
+            L.tzc_b200_tensor_text.argtypes = [C.c_char_p, C.c_int64, C.c_char_p, C.c_int64]
+            L.tzc_b200_tensor_roundtrip.argtypes = [C.c_char_p, C.c_char_p]
             L.tzc_b200_parse.argtypes = [C.c_char_p, C.c_char_p, C.c_int64]
             L.tzc_b200_inspect.argtypes = [C.c_char_p, C.c_char_p, C.c_int32, C.c_char_p, C.c_int64]
             L.tzc_b200_describe.argtypes = [C.c_char_p, C.c_char_p, C.c_char_p, C.c_int64]

@@ -178,3 +178,18 @@ extern "C" TZC_API int tzc_b200_eval_tir(const char* op_tdsl, const char* schedu
     return TZC_OK;
   });
 }
+
+extern "C" TZC_API int tzc_b200_tensor_text(const char* path, int64_t max_elems, char* buf, int64_t n) {
+  return guarded([&] {
+    if (!path) throw tzc::MissingInput("NULL path");
+    return put(tzc::tensor_to_text(tzc::load_tensor(path), max_elems), buf, n);
+  });
+}
+
+extern "C" TZC_API int tzc_b200_tensor_roundtrip(const char* src, const char* dst) {
+  return guarded([&] {
+    if (!src || !dst) throw tzc::MissingInput("NULL path");
+    tzc::save_tensor(dst, tzc::load_tensor(src));
+    return TZC_OK;
+  });
+}

@@ -663,7 +663,8 @@ TensorIR inject_intrinsic(const TensorIR& ir, const Intrinsic& intr, const LoopM
   }
   // The F6 pixel group (several op loops fused onto one instruction loop) is
   // realised by TMA im2col: its accesses stay scalar gather addresses.
-  const bool gather_ok = has_fused_group(mapping);
+  bool gather_ok = has_fused_group(mapping);
+  for (const auto& a : paxes) gather_ok = gather_ok || a.find(".fused") != std::string::npos;
 
   std::vector<ExprPtr> args;
   for (const auto& td : sem.tensors) {

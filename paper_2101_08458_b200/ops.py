@@ -73,6 +73,15 @@ def lower(op_text: str, schedule: str | None = None, intrinsic: str | None = Non
     return _text(lib().tzc_b200_lower, op_text.encode(), _enc(schedule), _enc(intrinsic))
 
 
+def tensor_text(path: str, max_elems: int = 64) -> str:
+    """tensor_to_text(load_tensor(path)) — the reference's TNSR container."""
+    return _text(lib().tzc_b200_tensor_text, path.encode(), max_elems)
+
+
+def tensor_roundtrip(src: str, dst: str) -> None:
+    check(lib().tzc_b200_tensor_roundtrip(src.encode(), dst.encode()))
+
+
 def eval_tir(op_text: str, intrinsic: str, inputs: dict, schedule: str | None = None, epilogue: str | None = None,
              out: np.ndarray | None = None):
     """The reference chain lower -> inject_intrinsic -> eval_tir, executed on the

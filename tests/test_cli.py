@@ -1,0 +1,87 @@
+"""The device CLI (paper_2101_08458_b200/tzc-b200) and the TNSR tensor
+container on CPU: files written by the reference's save_tensor read back to the
+reference's own tensor_to_text and re-save byte-identically; inspect /
+tensorize / error exit codes follow the reference CLI (proj/src/cli.cpp:41-47)."""
+import glob
+import os
+import shutil
+import subprocess
+import tempfile
+
+import pytest
+
+from oracle.pyoracle import Ref
+from paper_2101_08458_b200 import ops
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+CLI = os.path.join(ROOT, "paper_2101_08458_b200", "tzc-b200")
+TNSR = sorted(glob.glob(os.path.join(ROOT, "tests", "golden", "tnsr", "*", "*.tnsr")))
+needs_ref = pytest.mark.skipif(not Ref.available(), reason="oracle/_ref not built")
+needs_cli = pytest.mark.skipif(not os.path.exists(CLI), reason="tzc-b200 not built")
+
+
+def cli(*args):
+    p = subprocess.run([CLI, *args], capture_output=True, text=True, timeout=120)
+    return p.returncode, p.stdout, p.stderr
+
+
+def test_fixtures_present():
+    assert len(TNSR) >= 16
+
+
+@pytest.mark.parametrize("path", TNSR, ids=lambda p: "/".join(p.split("/")[-2:]))
+def test_container_roundtrip_is_byte_identical(path):
+    out = os.path.join(tempfile.mkdtemp(), "copy.tnsr")
+    ops.tensor_roundtrip(path, out)
+    assert open(out, "rb").read() == open(path, "rb").read()
+
+
+@needs_ref
+@pytest.mark.parametrize("path", TNSR, ids=lambda p: "/".join(p.split("/")[-2:]))
+def test_container_reads_like_the_reference(path):
+    assert ops.tensor_text(path, 1 << 30) == Ref.tensor_text(path)
+    assert ops.tensor_text(path) == Ref.tensor_text(path, 64)
+
+
+def test_container_errors(tmp_path):
+    bad = tmp_path / "bad.tnsr"
+    bad.write_bytes(b"NOPE\x01\x05\x01" + b"\x00" * 8)
+    with pytest.raises(Exception, match="IoError"):
+        ops.tensor_text(str(bad))
+    src = open(TNSR[0], "rb").read()
+    (tmp_path / "short.tnsr").write_bytes(src[:-1])
+    with pytest.raises(Exception, match="IoError"):
+        ops.tensor_text(str(tmp_path / "short.tnsr"), 1 << 30)
+
+
+@needs_cli
+def test_cli_inspect_and_tensorize():
+    d = os.path.join(ROOT, "tests", "golden", "tnsr", "conv_nhwc_i8")
+    op = os.path.join(d, "op.tdsl")
+    rc, out, _ = cli("inspect", op, "--intrinsic", "tcgen05_i8_m128n64k32")
+    assert rc == 0 and out.splitlines()[0] == "mapping 0: {(n,oh,ow)->m, k->n, c->k}"
+    sched = os.path.join(tempfile.mkdtemp(), "s.txt")
+    rc, out, _ = cli("tensorize", op, "--intrinsic", "tcgen05_i8_m128n64k32", "--schedule-out", sched)
+    assert rc == 0
+    assert out == ops.lower(open(op).read(), None, "tcgen05_i8_m128n64k32")
+    assert ops.lower(open(op).read(), open(sched).read(), "tcgen05_i8_m128n64k32").count("tcgen05_i8_m128n64k32(") == 1
+    rc, out, _ = cli("builtins")
+    assert rc == 0 and "tcgen05_i8_m128n256k32" in out.split()
+
+
+@needs_cli
+def test_cli_exit_codes(tmp_path):
+    d = os.path.join(ROOT, "tests", "golden", "tnsr", "mm_f16")
+    op = os.path.join(d, "op.tdsl")
+    assert cli("frobnicate")[0] == 2
+    assert cli("run", op)[0] == 2  # --intrinsic missing
+    (tmp_path / "bad.tdsl").write_text("tensor A : u8 [4] input\nnonsense\n")
+    assert cli("inspect", str(tmp_path / "bad.tdsl"), "--intrinsic", "vdot_16x4")[0] == 2
+    # float outputs need an explicit --rtol, as in the reference's verify
+    rc, _, err = cli("verify", op, "--intrinsic", "tcgen05_f16_m128n128k16_mn", "--expect", os.path.join(d, "expect.tnsr"))
+    assert rc == 2 and "rtol" in err
+    # a CPU instruction never executes (no CPU interpreter): domain failure
+    mm = os.path.join(ROOT, "tests", "golden", "tnsr", "mm_i8", "op.tdsl")
+    shutil.copy(mm, tmp_path / "mm.tdsl")
+    rc, _, err = cli("run", str(tmp_path / "mm.tdsl"), "--intrinsic", "vdot_16x4")
+    assert rc == 1 and "InjectError" in err
