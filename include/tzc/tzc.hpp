@@ -369,6 +369,11 @@ std::optional<LinearSplit> split_linear(const ExprPtr& e, const std::vector<std:
 
 struct LowerOptions {
   bool literal_unroll = false;
+  // Backend extension: a split whose factor does not divide the extent gets
+  // ceil(extent / factor) outer iterations instead of a ScheduleError; the
+  // device clips the tail (TMA out-of-bounds zero fill on loads, masked
+  // stores).  tensorized_ir sets it for fused pixel groups (F6).
+  bool clip_tails = false;
 };
 // Pad transforms throw PadUnsupported: this backend realises padding with
 // TMA out-of-bounds zero fill inside the kernel (tile_and_reorder's plan).

@@ -158,7 +158,7 @@ int cmd_tensorize(const Args& a, std::ostream& out) {
   const tzc::ComputeOp op = load_op(a);
   const tzc::Intrinsic intr = need_intrinsic(a);
   const tzc::TensorizedOp t = tzc::tensorize(op, intr);
-  out << tzc::print_tensor_ir(tzc::inject_intrinsic(tzc::lower(t.op, t.schedule), intr, t.mapping));
+  out << tzc::print_tensor_ir(tzc::tensorized_ir(op, intr));
   if (!a.schedule_out.empty()) {
     std::ofstream f(a.schedule_out);
     if (!f) throw tzc::IoError("cannot open '" + a.schedule_out + "' for writing");

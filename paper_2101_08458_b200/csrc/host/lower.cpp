@@ -367,6 +367,30 @@ TensorizedOp tile_and_reorder(const ComputeOp& op, const Intrinsic& intr, const 
   t.plan = plan_for(op, intr, mapping, mr.bind);
   // The reference schedule (split mapped loops by the instruction extents,
   // outer pieces outside, pragma over the inner pieces), recorded as text.
+  // Members of a fused group must be adjacent before they are fused: if the
+  // op declares them apart (conv2d_tdsl's ko ... ki), reorder first.
+  {
+    std::vector<std::string> order, seen;
+    for (const auto& l : op.loops) {
+      if (in(seen, l.name)) continue;
+      std::vector<std::string> group{l.name};
+      for (const auto& [o, i] : mapping.f) {
+        auto f = mapping.fused.find(i);
+        if (f == mapping.fused.end() || f->second.empty()) continue;
+        std::vector<std::string> members = f->second;
+        members.push_back(o);
+        if (in(members, l.name)) group = members;
+      }
+      for (const auto& g : group) order.push_back(g), seen.push_back(g);
+    }
+    bool moved = false;
+    for (size_t i = 0; i < order.size(); ++i) moved = moved || order[i] != op.loops[i].name;
+    if (moved) {
+      std::string ro = "reorder";
+      for (const auto& v : order) ro += " " + v;
+      t.schedule.push_back(ro);
+    }
+  }
   for (const auto& [o, i] : mapping.f) {
     const int64_t e = intr.semantics.find_loop(i)->extent;
     std::string axis = o;

@@ -269,12 +269,13 @@ ExprPtr zero_of(DType t) { return t.is_float() ? float_imm(0.0, t) : int_imm(0, 
 // the current axes, advanced one transform at a time.
 class Nest {
  public:
-  explicit Nest(const ComputeOp& op) {
+  explicit Nest(const ComputeOp& op, bool clip_tails) : clip(clip_tails) {
     for (const auto& l : op.loops) {
       axes.push_back({l.name, l.extent, l.kind});
       of[l.name] = var(l.name);
     }
   }
+  bool clip;
   std::vector<Axis> axes;
   std::map<std::string, ExprPtr> of;
   std::vector<std::string> pragma;
@@ -292,13 +293,13 @@ class Nest {
       case K::Split: {
         const size_t j = at(t.a, "split");
         const Axis ax = axes[j];
-        if (t.factor < 1 || ax.extent % t.factor)
+        if (t.factor < 1 || (ax.extent % t.factor && !clip))
           throw ScheduleError("split: factor " + std::to_string(t.factor) + " does not divide extent " +
                               std::to_string(ax.extent) + " of axis '" + t.a + "'");
         const std::string o = t.a + ".o", i = t.a + ".i";
         fresh(o, "split");
         fresh(i, "split");
-        axes[j] = {o, ax.extent / t.factor, ax.kind};
+        axes[j] = {o, (ax.extent + t.factor - 1) / t.factor, ax.kind};
         axes.insert(axes.begin() + j + 1, Axis{i, t.factor, ax.kind});
         rewrite({{t.a, add(mul(var(o), int_imm(t.factor)), var(i))}});
         break;
@@ -435,7 +436,7 @@ TensorIR lower(const ComputeOp& op, const Schedule& schedule, const LowerOptions
     throw PadUnsupported("pad '" + schedule.front().a +
                          "': this backend pads inside the kernel (TMA out-of-bounds zero fill); "
                          "use tile_and_reorder's plan");
-  Nest nest(op);
+  Nest nest(op, opts.clip_tails);
   for (const auto& t : schedule) nest.apply(t);
   nest.check_pragma_innermost();
 
@@ -735,7 +736,9 @@ TensorIR inject_intrinsic(const TensorIR& ir, const Intrinsic& intr, const LoopM
 
 TensorIR tensorized_ir(const ComputeOp& op, const Intrinsic& intr) {
   const TensorizedOp t = tensorize(op, intr);
-  return inject_intrinsic(lower(t.op, t.schedule), intr, t.mapping);
+  LowerOptions o;
+  o.clip_tails = has_fused_group(t.mapping);
+  return inject_intrinsic(lower(t.op, t.schedule, o), intr, t.mapping);
 }
 
 // ============================ eval_tir ===================================

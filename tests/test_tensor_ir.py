@@ -169,6 +169,12 @@ def test_fused_pixel_group_injects_as_gather():
     assert ".fused" in ir and " / " in ir and " % " in ir
     sched = ops.describe(text, "tcgen05_i8_m128n64k32")
     assert "fuse oh ow" in sched and "fuse n oh.ow.fused" in sched
+    # a pixel count that is not a multiple of 128: the tail tile is clipped on
+    # the device, so the outer loop takes ceil(100 / 128) = 1 iteration
+    ir = ops.lower(conv2d_tdsl(64, 12, 64, 3), None, "tcgen05_i8_m128n64k32")
+    assert "for oh.ow.fused.o : 1 {" in ir and ir.count("tcgen05_i8_m128n64k32(dst = ") == 1
+    with pytest.raises(TzcError, match="ScheduleError"):  # a user schedule stays strict
+        ops.lower(conv2d_tdsl(64, 12, 64, 3), "fuse oh ow\nsplit oh.ow.fused 128\n")
 
 
 def test_lowering_errors():
