@@ -53,6 +53,9 @@ def parse():
     ap.add_argument("--profile", default="i8", choices=["i8", "f16"],
                     help="i8: the BASELINE metric (default); f16: configs[3] (fp16 in, fp32 accumulate, fp16 out)")
     ap.add_argument("--opt", action="append", default=[], help="name=value passed to tzc_b200_set_option (tuning)")
+    ap.add_argument("--tune", type=int, default=0,
+                    help="1: measured-time plan search per layer (tzc_b200_tune_conv) before graph capture")
+    ap.add_argument("--tune-reps", type=int, default=10)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-threads", type=int, default=3, help="host threads issuing run_op calls in the e2e leg")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -261,6 +264,19 @@ def run_ours(args, rank, world, local):
         suite(False)
         suite_branches()
     torch.cuda.synchronize()
+    tuned = {}
+    if args.tune:
+        # measured-time plan per layer (outside every timed region); the
+        # winners are installed for these descriptors and baked into the graphs
+        for b in bufs:
+            best, log = D.tune_conv2d(b["x"], b["w"], b["layer"].stride, epilogue=b["ep"], scale=b["scale"],
+                                      out=b["out"], stream=stream, reps=args.tune_reps)
+            last = log.strip().splitlines()[-1]
+            tuned[b["layer"].name] = last.split(" ", 2)[2] if best else "default"
+        with torch.cuda.stream(stream):
+            suite(False)
+            suite_branches()
+        torch.cuda.synchronize()
     # graph A: the timed step (no per-layer events inside);
     # graph B: the same launches with cudaEventRecordExternal events around
     # every layer, replayed after the timed region for the per-layer table
@@ -352,7 +368,8 @@ def run_ours(args, rank, world, local):
                    "algo_bytes_per_step_per_gpu": bytes_step,
                    "l2": "flushed (512 MiB memset) between timed steps, outside the timed events",
                    "parallelism": f"dp{world} (batch-sharded, no collective)",
-                   "graph_branches": args.branches},
+                   "graph_branches": args.branches,
+                   **({"tuned_plans": tuned} if args.tune else {})},
         "pct_of_spec_peak": round(100.0 * value / (spec * world), 2),
         "gpu_launches": launches_per_step * args.steps,
         "clocks": clk.summary(),

@@ -184,6 +184,26 @@ TZC_API int tzc_b200_unblock_data(const void* src, void* dst, int32_t c, int32_t
 TZC_API int tzc_b200_unblock_kernel(const void* src, void* dst, int32_t k, int32_t c, int32_t r,
                             int32_t s, int32_t kb, int32_t cb, int32_t elem_bytes, void* stream);
 
+/* Measured-time tuner (the device analogue of tzc::tune, proj/include/tzc/
+ * tuner.hpp:71-72 / proj/src/tuner.cpp:111-274, which ranks candidates by a
+ * VM cost model): times each candidate kernel plan of this problem (tile
+ * width, split-K, kernel family, tiles per unit, epilogue grouping, store
+ * path, CTA pairs) with CUDA events over `reps` launches on `stream` (L2-warm,
+ * the caller's buffers; results never change between plans), writes one
+ * "candidate <i> <options> <us> us" line per candidate plus a "best" line into
+ * `log`, and returns the winning index (0 = the default plan; a non-default
+ * plan must be >= 1% faster).  With apply != 0 the winner is installed for
+ * every later launch of an identical descriptor (also inside CUDA graphs
+ * captured afterwards).  The stream must not be capturing. */
+TZC_API int tzc_b200_tune_conv(const tzc_conv_desc* d, const void* x, const void* w, const void* c_seed, void* out,
+                               const tzc_epilogue* ep, int32_t reps, int32_t apply, char* log, int64_t loglen,
+                               void* stream);
+TZC_API int tzc_b200_tune_gemm(const tzc_gemm_desc* d, const void* a, const void* b, const void* c_seed, void* out,
+                               const tzc_epilogue* ep, int32_t reps, int32_t apply, char* log, int64_t loglen,
+                               void* stream);
+/* Drops every installed per-problem plan. */
+TZC_API int tzc_b200_clear_tuning(void);
+
 /* ---- level 2: op text + host buffers (reference-facing plugin) -------------- */
 /* Runs `op_tdsl` tensorized with `intrinsic` (a builtin name such as
  * "tcgen05_i8_m128n256k32" or a .intr path) on the GPU.  Inputs are HOST

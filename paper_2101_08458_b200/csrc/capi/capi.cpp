@@ -4,6 +4,9 @@
 #include <cuda_runtime.h>
 
 #include <cstring>
+#include <map>
+#include <mutex>
+#include <vector>
 #include <exception>
 #include <string>
 
@@ -129,6 +132,62 @@ using namespace tzcb200;
 
 namespace {
 
+int set_option_raw(const std::string& n, int64_t value);
+
+// Process-wide option values (the defaults of conv_tc.cu) and per-problem
+// overrides installed by the measured tuner (tzc_b200_tune_*): a launch whose
+// descriptor has an entry runs with those options, then the process values
+// come back.  Options change the kernel plan only, never the results.
+std::mutex g_opt_mu;
+std::map<std::string, int64_t> g_opt_now = {
+    {"splits", 0},      {"shifted_window", 1}, {"ws_epi_groups", 1}, {"tail_split", 0}, {"split_min_kb", 1 << 20},
+    {"pingpong_kb", 2}, {"ws_mt", 0},          {"ws_1x1_k", 64},     {"ws_1x1", 0},     {"bn", 0},
+    {"tma_store_k", 64}, {"pair_min_kb", 16},  {"pair", 0},          {"st256", 1},      {"l2_hints", 1},
+    {"tma_store", 0}};
+using Overrides = std::vector<std::pair<std::string, int64_t>>;
+std::map<std::string, Overrides> g_problem_opts;
+
+template <typename D>
+std::string key_of(const D& d, char kind) {
+  return std::string(1, kind) + std::string(reinterpret_cast<const char*>(&d), sizeof(D));
+}
+
+class ScopedOptions {
+ public:
+  explicit ScopedOptions(const Overrides& o) : lk_(g_opt_mu, std::defer_lock), o_(o) {
+    if (o_.empty()) return;
+    lk_.lock();
+    for (const auto& [n, v] : o_) set_option_raw(n, v);
+  }
+  ~ScopedOptions() {
+    for (const auto& [n, v] : o_) set_option_raw(n, g_opt_now[n]);
+  }
+
+ private:
+  std::unique_lock<std::mutex> lk_;
+  Overrides o_;
+};
+
+Overrides overrides_for(const std::string& key) {
+  std::lock_guard<std::mutex> lk(g_opt_mu);
+  auto it = g_problem_opts.find(key);
+  return it == g_problem_opts.end() ? Overrides{} : it->second;
+}
+
+Overrides parse_overrides(const std::string& spec) {
+  Overrides o;
+  size_t i = 0;
+  while (i < spec.size()) {
+    size_t j = spec.find(';', i);
+    if (j == std::string::npos) j = spec.size();
+    const std::string kv = spec.substr(i, j - i);
+    const size_t eq = kv.find('=');
+    if (eq != std::string::npos) o.emplace_back(kv.substr(0, eq), std::stoll(kv.substr(eq + 1)));
+    i = j + 1;
+  }
+  return o;
+}
+
 int run_conv(const tzc_conv_desc* d, int profile, const void* x, const void* w, const void* seed, void* out,
              const tzc_epilogue* ep, void* stream) {
   if (!d || !ep) return report(Status(TZC_E_MISSING_INPUT, "NULL descriptor"));
@@ -140,6 +199,7 @@ int run_conv(const tzc_conv_desc* d, int profile, const void* x, const void* w, 
   if (st.ok()) st = check_ptr(seed, "c_seed", true, false);
   if (st.ok()) st = check_ptr(out, "out", false, false);
   if (!st.ok()) return report(st);
+  ScopedOptions so(overrides_for(key_of(*d, 'c')));
   return report(run_problem(pb, x, w, seed, out, *ep, static_cast<cudaStream_t>(stream)));
 }
 
@@ -154,6 +214,7 @@ int run_gemm(const tzc_gemm_desc* d, int profile, const void* a, const void* b, 
   if (st.ok()) st = check_ptr(seed, "c_seed", true, false);
   if (st.ok()) st = check_ptr(out, "out", false, false);
   if (!st.ok()) return report(st);
+  ScopedOptions so(overrides_for(key_of(*d, 'g')));
   return report(run_problem(pb, a, b, seed, out, *ep, static_cast<cudaStream_t>(stream)));
 }
 
@@ -209,9 +270,11 @@ int tzc_b200_plan_gemm(const tzc_gemm_desc* d, tzc_plan* plan) {
   TZC_GUARD_END
 }
 
-int tzc_b200_set_option(const char* name, int64_t value) {
-  if (!name) return report(Status(TZC_E_MISSING_INPUT, "NULL option name"));
-  const std::string n(name);
+}  // extern "C"
+
+namespace {
+
+int set_option_raw(const std::string& n, int64_t value) {
   if (n == "splits") {
     if (value < 0) return report(Status(TZC_E_SHAPE, "splits must be >= 0"));
     set_forced_splits((int)value);
@@ -280,6 +343,18 @@ int tzc_b200_set_option(const char* name, int64_t value) {
   return report(Status(TZC_E_VALIDATION, "unknown option '" + n + "'"));
 }
 
+}  // namespace
+
+extern "C" {
+
+int tzc_b200_set_option(const char* name, int64_t value) {
+  if (!name) return report(Status(TZC_E_MISSING_INPUT, "NULL option name"));
+  std::lock_guard<std::mutex> lk(g_opt_mu);
+  const int rc = set_option_raw(name, value);
+  if (rc == TZC_OK) g_opt_now[name] = value;
+  return rc;
+}
+
 int tzc_b200_set_splits(int32_t splits) {
   if (splits < 0) return report(Status(TZC_E_SHAPE, "splits must be >= 0"));
   set_forced_splits(splits);
@@ -315,5 +390,128 @@ int tzc_b200_device_ok(void) {
 }
 
 const char* tzc_b200_version(void) { return "tzc-b200 0.1.0 (sm_100a, tcgen05 kind::i8/kind::f16)"; }
+
+}  // extern "C"
+
+// ---- measured-time tuner (the device analogue of tzc::tune, proj/src/tuner.cpp:111-274) ----
+namespace {
+
+// Candidate option sets; index 0 is the default plan.  Each is one kernel-plan
+// decision of the reference's GPU sketch space re-cast for this backend:
+// tile width (BN), split-K (split_reduction), kernel family (shifted window vs
+// TMA im2col), tiles per work unit, epilogue grouping, store path, CTA pairs.
+const char* const kCandidates[] = {
+    "",           "bn=64",          "bn=128",         "bn=256",        "splits=2",      "splits=4",
+    "shifted_window=0", "ws_mt=1",  "ws_mt=2",        "ws_mt=4",       "pingpong_kb=0", "pingpong_kb=16",
+    "tma_store=1", "pair=1;pair_min_kb=1", "ws_1x1=1", "ws_epi_groups=2", "l2_hints=0"};
+constexpr int kNumCandidates = sizeof(kCandidates) / sizeof(kCandidates[0]);
+
+template <typename Run>
+int tune_problem(const std::string& key, Run run, int reps, int apply, char* log, int64_t loglen, cudaStream_t st) {
+  if (reps < 1) reps = 10;
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(st, &cap) == cudaSuccess && cap != cudaStreamCaptureStatusNone)
+    return report(Status(TZC_E_VALIDATION, "tune: the stream is being captured"));
+  cudaEvent_t e0, e1;
+  if (cudaEventCreate(&e0) != cudaSuccess || cudaEventCreate(&e1) != cudaSuccess)
+    return report(Status(TZC_E_DEVICE, "tune: cudaEventCreate failed"));
+  std::string text;
+  double best_us = 0, default_us = 0;
+  int best = -1;
+  for (int c = 0; c < kNumCandidates; ++c) {
+    const Overrides o = parse_overrides(kCandidates[c]);
+    float ms = 0;
+    Status s;
+    {
+      ScopedOptions so(o);
+      for (int w = 0; w < 2 && s.ok(); ++w) s = run(st);
+      if (s.ok()) cudaEventRecord(e0, st);
+      for (int r = 0; r < reps && s.ok(); ++r) s = run(st);
+      if (s.ok()) cudaEventRecord(e1, st);
+      if (s.ok() && cudaEventSynchronize(e1) != cudaSuccess) s = Status(TZC_E_DEVICE, "tune: launch failed");
+      if (s.ok()) cudaEventElapsedTime(&ms, e0, e1);
+    }
+    char line[160];
+    if (!s.ok()) {
+      if (c == 0) {
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        return report(s);
+      }
+      std::snprintf(line, sizeof line, "candidate %d %s skipped\n", c, kCandidates[c]);
+      text += line;
+      continue;
+    }
+    const double us = 1000.0 * ms / reps;
+    std::snprintf(line, sizeof line, "candidate %d %s %.2f us\n", c, c ? kCandidates[c] : "default", us);
+    text += line;
+    if (c == 0) default_us = us;
+    // a non-default plan must beat the default by 1% to be kept
+    if (best < 0 || (us < best_us && us < 0.99 * default_us)) best = c, best_us = us;
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  char line[160];
+  std::snprintf(line, sizeof line, "best %d %s %.2f us (default %.2f us)\n", best, best ? kCandidates[best] : "default",
+                best_us, default_us);
+  text += line;
+  if (apply) {
+    std::lock_guard<std::mutex> lk(g_opt_mu);
+    if (best) g_problem_opts[key] = parse_overrides(kCandidates[best]);
+    else g_problem_opts.erase(key);
+  }
+  if (log && loglen > 0) {
+    const size_t n = std::min<size_t>(text.size(), (size_t)loglen - 1);
+    std::memcpy(log, text.data(), n);
+    log[n] = 0;
+  }
+  return best;
+}
+
+}  // namespace
+
+extern "C" {
+
+int tzc_b200_tune_conv(const tzc_conv_desc* d, const void* x, const void* w, const void* c_seed, void* out,
+                       const tzc_epilogue* ep, int32_t reps, int32_t apply, char* log, int64_t loglen, void* stream) {
+  TZC_GUARD_BEGIN
+  if (!d || !ep) return report(Status(TZC_E_MISSING_INPUT, "NULL descriptor"));
+  Problem pb;
+  Status st = problem_from_conv(*d, &pb);
+  if (st.ok()) st = check_ptr(x, "x", false);
+  if (st.ok()) st = check_ptr(w, "w", false);
+  if (st.ok()) st = check_ptr(c_seed, "c_seed", true, false);
+  if (st.ok()) st = check_ptr(out, "out", false, false);
+  if (!st.ok()) return report(st);
+  const tzc_epilogue e = *ep;
+  return tune_problem(
+      key_of(*d, 'c'), [&](cudaStream_t s) { return run_problem(pb, x, w, c_seed, out, e, s); }, reps, apply, log,
+      loglen, static_cast<cudaStream_t>(stream));
+  TZC_GUARD_END
+}
+
+int tzc_b200_tune_gemm(const tzc_gemm_desc* d, const void* a, const void* b, const void* c_seed, void* out,
+                       const tzc_epilogue* ep, int32_t reps, int32_t apply, char* log, int64_t loglen, void* stream) {
+  TZC_GUARD_BEGIN
+  if (!d || !ep) return report(Status(TZC_E_MISSING_INPUT, "NULL descriptor"));
+  Problem pb;
+  Status st = problem_from_gemm(*d, &pb);
+  if (st.ok()) st = check_ptr(a, "a", false);
+  if (st.ok()) st = check_ptr(b, "b", false);
+  if (st.ok()) st = check_ptr(c_seed, "c_seed", true, false);
+  if (st.ok()) st = check_ptr(out, "out", false, false);
+  if (!st.ok()) return report(st);
+  const tzc_epilogue e = *ep;
+  return tune_problem(
+      key_of(*d, 'g'), [&](cudaStream_t s) { return run_problem(pb, a, b, c_seed, out, e, s); }, reps, apply, log,
+      loglen, static_cast<cudaStream_t>(stream));
+  TZC_GUARD_END
+}
+
+int tzc_b200_clear_tuning(void) {
+  std::lock_guard<std::mutex> lk(g_opt_mu);
+  g_problem_opts.clear();
+  return TZC_OK;
+}
 
 }  // extern "C"

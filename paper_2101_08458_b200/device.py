@@ -96,6 +96,49 @@ def gemm(a, b, seed=None, epilogue="i32", scale=1.0, out=None, b_kn=False, out_l
     return out
 
 
+def tune_conv2d(x, w, stride=1, seed=None, epilogue="i32", scale=1.0, out=None, w_layout="krsc",
+                out_layout=None, out_shape=None, stream=None, reps=10, apply=True):
+    """Measured-time plan search for this conv (tzc_b200_tune_conv): returns
+    (best candidate index, log text); with ``apply`` later launches of the same
+    descriptor use the winner."""
+    f16 = x.dtype == torch.float16
+    d, shape = conv_desc(tuple(x.shape), tuple(w.shape), stride, f16, w_layout, out_layout)
+    kind = EPILOGUES[epilogue]
+    if out is None:
+        out = torch.empty(out_shape or shape, dtype=_OUT_DTYPE[kind], device=x.device)
+    ep = Epilogue(kind=kind, scale=scale)
+    log = C.create_string_buffer(1 << 14)
+    best = lib().tzc_b200_tune_conv(C.byref(d), _ptr(x), _ptr(w), _ptr(seed), _ptr(out), C.byref(ep), int(reps),
+                                    int(apply), log, len(log), _stream(stream))
+    if best < 0:
+        check(best)
+    return best, log.value.decode()
+
+
+def tune_gemm(a, b, seed=None, epilogue="i32", scale=1.0, out=None, b_kn=False, out_layout=None, stream=None,
+              reps=10, apply=True):
+    """As :func:`tune_conv2d` for a matmul (tzc_b200_tune_gemm)."""
+    f16 = a.dtype == torch.float16
+    m, k = a.shape
+    n = b.shape[1] if b_kn else b.shape[0]
+    d = GemmDesc(profile=PROFILE_F16 if f16 else PROFILE_U8I8, m=m, n=n, k=k, b_kn=int(b_kn))
+    d.out = out_layout if out_layout is not None else nhwc_layout(n)
+    kind = EPILOGUES[epilogue]
+    if out is None:
+        out = torch.empty((m, n), dtype=_OUT_DTYPE[kind], device=a.device)
+    ep = Epilogue(kind=kind, scale=scale)
+    log = C.create_string_buffer(1 << 14)
+    best = lib().tzc_b200_tune_gemm(C.byref(d), _ptr(a), _ptr(b), _ptr(seed), _ptr(out), C.byref(ep), int(reps),
+                                    int(apply), log, len(log), _stream(stream))
+    if best < 0:
+        check(best)
+    return best, log.value.decode()
+
+
+def clear_tuning():
+    check(lib().tzc_b200_clear_tuning())
+
+
 def unblock_data(src, c, h, w, cb, stream=None):
     dst = torch.empty((1, h, w, c), dtype=src.dtype, device=src.device)
     check(lib().tzc_b200_unblock_data(_ptr(src), _ptr(dst), c, h, w, cb, src.element_size(), _stream(stream)))

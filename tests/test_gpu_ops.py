@@ -147,3 +147,27 @@ def test_eval_tir_blocked_c1_matches_reference_sha(cuda):
     ins = Orc.random_inputs(decls(text), int(g["seed"]))
     out = ops.eval_tir(text, "tcgen05_i8_m128n64k32", ins)
     assert hashlib.sha256(out.tobytes()).hexdigest() == str(g["sha_i32"])
+
+
+# ---- measured-time tuner (tzc_b200_tune_conv / _gemm) ----
+def test_tuner_installs_a_plan_and_results_stay_exact(cuda):
+    import torch
+
+    from paper_2101_08458_b200 import device as D
+    dev = torch.device("cuda:0")
+    x = torch.from_numpy(Orc.random_tensor("u8", (4, 16, 16, 64), 3)).to(dev)
+    w = torch.from_numpy(Orc.random_tensor("i8", (128, 3, 3, 64), 4)).to(dev)
+    ref = Orc.conv2d_nhwc(x.cpu().numpy(), w.cpu().numpy(), 1)
+    try:
+        best, log = D.tune_conv2d(x, w, 1, epilogue="requant_i8", scale=2.0 ** -12, reps=3)
+        lines = log.strip().splitlines()
+        assert sum(ln.startswith("candidate ") for ln in lines) == 17 and lines[-1].startswith(f"best {best} ")
+        assert 0 <= best < 17
+        q = D.conv2d(x, w, 1, epilogue="requant_i8", scale=2.0 ** -12).cpu().numpy()
+        assert np.array_equal(q, Orc.requant_i8(ref, 2.0 ** -12))
+        a = torch.from_numpy(Orc.random_tensor("u8", (384, 256), 5)).to(dev)
+        b = torch.from_numpy(Orc.random_tensor("i8", (512, 256), 6)).to(dev)
+        best, _ = D.tune_gemm(a, b, reps=3)
+        assert np.array_equal(D.gemm(a, b).cpu().numpy(), Orc.matmul(a.cpu().numpy(), b.cpu().numpy()))
+    finally:
+        D.clear_tuning()
