@@ -203,6 +203,13 @@ TZC_API int tzc_b200_tune_gemm(const tzc_gemm_desc* d, const void* a, const void
                                void* stream);
 /* Drops every installed per-problem plan. */
 TZC_API int tzc_b200_clear_tuning(void);
+/* Installs ("name=value;...") or clears ("" / NULL) the plan options for every
+ * launch of this exact descriptor — how a suite-level search (bench.py
+ * --tune 2) applies its per-layer choices. */
+TZC_API int tzc_b200_set_problem_options_conv(const tzc_conv_desc* d, const char* spec);
+TZC_API int tzc_b200_set_problem_options_gemm(const tzc_gemm_desc* d, const char* spec);
+/* The candidate option specs tzc_b200_tune_* times, one per line (line 0 = default). */
+TZC_API int tzc_b200_tune_candidates(char* buf, int64_t buflen);
 
 /* ---- level 2: op text + host buffers (reference-facing plugin) -------------- */
 /* Runs `op_tdsl` tensorized with `intrinsic` (a builtin name such as

@@ -30,6 +30,7 @@ EXPORTS = (
     "tzc_b200_unblock_data", "tzc_b200_unblock_kernel", "tzc_b200_run_op", "tzc_b200_eval_tir", "tzc_b200_lower",
     "tzc_b200_tensor_text", "tzc_b200_tensor_roundtrip",
     "tzc_b200_tune_conv", "tzc_b200_tune_gemm", "tzc_b200_clear_tuning",
+    "tzc_b200_set_problem_options_conv", "tzc_b200_set_problem_options_gemm", "tzc_b200_tune_candidates",
     "tzc_b200_parse", "tzc_b200_inspect", "tzc_b200_describe", "tzc_b200_builtins",
     "tzc_b200_print_intrinsic",
     "tzc_b200_last_error", "tzc_b200_launch_count", "tzc_b200_device_ok", "tzc_b200_version",
@@ -99,6 +100,9 @@ def lib():
             for fn, desc in (("tzc_b200_tune_conv", ConvDesc), ("tzc_b200_tune_gemm", GemmDesc)):
                 getattr(L, fn).argtypes = [C.POINTER(desc), P, P, P, P, C.POINTER(Epilogue), C.c_int32, C.c_int32,
                                            C.c_char_p, C.c_int64, P]
+            L.tzc_b200_set_problem_options_conv.argtypes = [C.POINTER(ConvDesc), C.c_char_p]
+            L.tzc_b200_set_problem_options_gemm.argtypes = [C.POINTER(GemmDesc), C.c_char_p]
+            L.tzc_b200_tune_candidates.argtypes = [C.c_char_p, C.c_int64]
             L.tzc_b200_plan_conv.argtypes = [C.POINTER(ConvDesc), C.POINTER(Plan)]
             L.tzc_b200_plan_gemm.argtypes = [C.POINTER(GemmDesc), C.POINTER(Plan)]
             L.tzc_b200_set_splits.argtypes = [C.c_int32]

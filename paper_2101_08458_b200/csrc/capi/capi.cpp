@@ -515,3 +515,44 @@ int tzc_b200_clear_tuning(void) {
 }
 
 }  // extern "C"
+
+extern "C" {
+
+// Installs (spec = "name=value;...") or clears (spec = "" or NULL) the plan
+// options used for every launch of this exact descriptor.
+int tzc_b200_set_problem_options_conv(const tzc_conv_desc* d, const char* spec) {
+  TZC_GUARD_BEGIN
+  if (!d) return report(Status(TZC_E_MISSING_INPUT, "NULL descriptor"));
+  const Overrides o = parse_overrides(spec ? spec : "");
+  for (const auto& kv : o)
+    if (!g_opt_now.count(kv.first)) return report(Status(TZC_E_VALIDATION, "unknown option '" + kv.first + "'"));
+  std::lock_guard<std::mutex> lk(g_opt_mu);
+  if (o.empty()) g_problem_opts.erase(key_of(*d, 'c'));
+  else g_problem_opts[key_of(*d, 'c')] = o;
+  return TZC_OK;
+  TZC_GUARD_END
+}
+
+int tzc_b200_set_problem_options_gemm(const tzc_gemm_desc* d, const char* spec) {
+  TZC_GUARD_BEGIN
+  if (!d) return report(Status(TZC_E_MISSING_INPUT, "NULL descriptor"));
+  const Overrides o = parse_overrides(spec ? spec : "");
+  for (const auto& kv : o)
+    if (!g_opt_now.count(kv.first)) return report(Status(TZC_E_VALIDATION, "unknown option '" + kv.first + "'"));
+  std::lock_guard<std::mutex> lk(g_opt_mu);
+  if (o.empty()) g_problem_opts.erase(key_of(*d, 'g'));
+  else g_problem_opts[key_of(*d, 'g')] = o;
+  return TZC_OK;
+  TZC_GUARD_END
+}
+
+// The tuner's candidate plans, one option spec per line (line 0 = default = "").
+int tzc_b200_tune_candidates(char* buf, int64_t buflen) {
+  std::string s;
+  for (int c = 0; c < kNumCandidates; ++c) s += std::string(kCandidates[c]) + "\n";
+  if (!buf || (int64_t)s.size() + 1 > buflen) return report(Status(TZC_E_SHAPE, "text buffer too small"));
+  std::memcpy(buf, s.c_str(), s.size() + 1);
+  return TZC_OK;
+}
+
+}  // extern "C"

@@ -135,6 +135,18 @@ def tune_gemm(a, b, seed=None, epilogue="i32", scale=1.0, out=None, b_kn=False, 
     return best, log.value.decode()
 
 
+def tune_candidates() -> list:
+    buf = C.create_string_buffer(1 << 12)
+    check(lib().tzc_b200_tune_candidates(buf, len(buf)))
+    return buf.value.decode().split("\n")[:-1]
+
+
+def set_conv_plan(x_shape, w_shape, stride=1, f16=False, w_layout="krsc", out_layout=None, spec=""):
+    """Install (or clear, spec="") per-descriptor plan options for this conv."""
+    d, _ = conv_desc(tuple(x_shape), tuple(w_shape), stride, f16, w_layout, out_layout)
+    check(lib().tzc_b200_set_problem_options_conv(C.byref(d), spec.encode()))
+
+
 def clear_tuning():
     check(lib().tzc_b200_clear_tuning())
 
