@@ -53,9 +53,11 @@ def parse():
     ap.add_argument("--profile", default="i8", choices=["i8", "f16"],
                     help="i8: the BASELINE metric (default); f16: configs[3] (fp16 in, fp32 accumulate, fp16 out)")
     ap.add_argument("--opt", action="append", default=[], help="name=value passed to tzc_b200_set_option (tuning)")
-    ap.add_argument("--tune", type=int, default=2,
+    ap.add_argument("--tune", type=int, default=-1,
                     help="plan search before graph capture (never inside the timed region): 0 off, 1 per layer "
-                         "in isolation (tzc_b200_tune_conv), 2 per layer against the whole multi-branch step")
+                         "in isolation (tzc_b200_tune_conv), 2 per layer against the whole multi-branch step; "
+                         "-1 (auto) = 2 when a rank holds <= 64 images (layers leave SMs idle, plans matter), "
+                         "else 0 (at 256 the search kept every default in 3/3 runs and only heated the GPU)")
     ap.add_argument("--tune-reps", type=int, default=10)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-threads", type=int, default=3, help="host threads issuing run_op calls in the e2e leg")
@@ -315,6 +317,8 @@ def run_ours(args, rank, world, local):
         suite_branches()
     torch.cuda.synchronize()
     tuned = {}
+    if args.tune < 0:
+        args.tune = 2 if bpg <= 64 else 0
     if args.tune == 1:
         # measured-time plan per layer (outside every timed region); the
         # winners are installed for these descriptors and baked into the graphs
@@ -333,6 +337,7 @@ def run_ours(args, rank, world, local):
             suite(False)
             suite_branches()
         torch.cuda.synchronize()
+        time.sleep(2.0)  # let the power controller settle after the search's back-to-back replays
     # graph A: the timed step (no per-layer events inside);
     # graph B: the same launches with cudaEventRecordExternal events around
     # every layer, replayed after the timed region for the per-layer table
@@ -425,6 +430,7 @@ def run_ours(args, rank, world, local):
                    "l2": "flushed (512 MiB memset) between timed steps, outside the timed events",
                    "parallelism": f"dp{world} (batch-sharded, no collective)",
                    "graph_branches": args.branches,
+                   "plan_search": {0: "off", 1: "per layer, isolated", 2: "per layer, whole step"}[args.tune],
                    **({"tuned_plans": tuned} if args.tune else {})},
         "pct_of_spec_peak": round(100.0 * value / (spec * world), 2),
         "gpu_launches": launches_per_step * args.steps,
