@@ -116,3 +116,17 @@ def test_plan_stem_space_to_depth():
     d, _ = D.conv_desc((256, L.h, L.h, L.c), (L.k, L.r, L.r, L.c), L.stride)
     p = D.plan_conv(d)
     assert p["a_mode"] == 3 and p["bk_bytes"] == 16 and p["bn"] == 64
+
+
+def test_problem_options_validation_and_candidates():
+    """Per-descriptor plan options (the tuner's install path) need no device:
+    unknown names are rejected, known ones install and clear."""
+    from paper_2101_08458_b200 import device as D
+    from paper_2101_08458_b200._capi import TzcError
+    cands = D.tune_candidates()
+    assert cands[0] == "" and len(cands) == 17 and "bn=128" in cands
+    D.set_conv_plan((2, 10, 10, 64), (64, 3, 3, 64), 1, spec="bn=128;pingpong_kb=0")
+    D.set_conv_plan((2, 10, 10, 64), (64, 3, 3, 64), 1, spec="")
+    with pytest.raises(TzcError, match="unknown option"):
+        D.set_conv_plan((2, 10, 10, 64), (64, 3, 3, 64), 1, spec="warp_speed=9")
+    D.clear_tuning()

@@ -171,3 +171,18 @@ def test_tuner_installs_a_plan_and_results_stay_exact(cuda):
         assert np.array_equal(D.gemm(a, b).cpu().numpy(), Orc.matmul(a.cpu().numpy(), b.cpu().numpy()))
     finally:
         D.clear_tuning()
+
+
+def test_eval_tir_random_reference_schedules(cuda):
+    """Seeded random tcgen05 schedules (reordered / annotated outer loops,
+    split_reduction) lowered, injected and executed: bit-exact every time."""
+    import random
+
+    from tests.test_tensor_ir import random_tcgen05_schedule
+    text = matmul_tdsl(256, 256, 128)
+    ins = Orc.random_inputs(decls(text), 19)
+    ref = Orc.matmul(ins["A"], ins["B"], ins["C"])
+    rng = random.Random(7)
+    for _ in range(6):
+        sched = random_tcgen05_schedule(rng)
+        assert np.array_equal(ops.eval_tir(text, "tcgen05_i8_m128n128k32", ins, schedule=sched), ref), sched

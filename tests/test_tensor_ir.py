@@ -198,3 +198,38 @@ def test_eval_tir_has_no_cpu_interpreter():
     ins = {"A": np.zeros((32, 8), np.uint8), "B": np.zeros((32, 8), np.int8), "C": np.zeros((32, 32), np.int32)}
     with pytest.raises(TzcError, match="InjectError"):
         ops.eval_tir(text, intr, ins, schedule=sched)
+
+
+def random_tcgen05_schedule(rng, n=128):
+    """Split onto tcgen05's (m, n, k) = (128, n, 32) pragma nest; the outer axes
+    are shuffled and annotated at random (split_reduction on k.o included)."""
+    outer = ["x.o", "y.o", "k.o"]
+    lines = ["split x 128", f"split y {n}", "split k 32"]
+    if rng.random() < 0.4:
+        lines.append("split_reduction k.o 2")
+        outer = ["x.o", "y.o", "k.o.s", "k.o.r"]
+    rng.shuffle(outer)
+    lines.append("reorder " + " ".join(outer + ["x.i", "y.i", "k.i"]))
+    for a in outer:
+        r = rng.random()
+        if r < 0.25 and not a.startswith("k.o.r") and a != "k.o":
+            lines.append(f"parallel {a}")
+        elif r < 0.45:
+            lines.append(f"unroll {a}")
+    lines.append("pragma x.i y.i k.i")
+    return "\n".join(lines) + "\n"
+
+
+@needs_ref
+def test_random_tcgen05_schedules_inject_like_the_reference():
+    text = matmul_tdsl(256, 256, 128)
+    intr = "tcgen05_i8_m128n128k32"
+    path = os.path.join(tempfile.mkdtemp(), f"{intr}.intr")
+    with open(path, "w") as f:
+        f.write(ops.print_intrinsic(intr))
+    rng = random.Random(7)
+    for _ in range(12):
+        sched = random_tcgen05_schedule(rng)
+        ours, ref = _both(lambda: ops.lower(text, sched, intr), lambda: Ref.lower(text, sched, path))
+        assert not isinstance(ref, tuple), (sched, ref)
+        assert ours == ref, sched
