@@ -283,6 +283,7 @@ struct KernelPlan {
   int64_t cb = 0, kb = 0;         // ConvBlocked: channel blocks of data / output
   int64_t out_nb = 0, out_stride_m = 0, out_stride_blk = 0;
   std::string data, weight, out;  // op tensor names bound to a, b, d
+  int64_t splits = 0;             // device split-K from the schedule's split_reduction (0 = planner's choice)
   std::string describe() const;
 };
 struct TensorizedOp {

@@ -582,6 +582,7 @@ void run_tensorized_packed(const TensorizedOp& t, const std::map<std::string, co
       s = problem_from_conv(c, &pb);
     }
     if (!s.ok()) throw InjectError(s.msg);
+    pb.forced_splits = (int)p.splits;
     return pb;
   };
 

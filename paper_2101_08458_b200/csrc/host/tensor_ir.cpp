@@ -758,8 +758,14 @@ TensorizedOp device_plan(const TensorIR& ir) {
   if (!ir.source) throw InjectError("TensorIR was not lowered by this library (no source op)");
   // The schedule fixes a loop order; the kernel computes the same function
   // (bit-exact for integers by wrap-add associativity, F8; within 1e-3 for fp16).
-  if (!ir.mapping.f.empty()) return tile_and_reorder(*ir.source, *intr, ir.mapping, true);
-  return tensorize(*ir.source, *intr);
+  TensorizedOp t = ir.mapping.f.empty() ? tensorize(*ir.source, *intr)
+                                         : tile_and_reorder(*ir.source, *intr, ir.mapping, true);
+  // split_reduction (rewriter.cpp:425-451) becomes the device split-K: the
+  // segment count of the partial buffer is the number of K splits, folded by
+  // the wrap-add fix-up kernel (exact for integers, F8).
+  for (const auto& name : ir.temps)
+    if (const TensorDecl* d = ir.find_tensor(name)) t.plan.splits = d->shape.front();
+  return t;
 }
 
 TensorValue eval_tir(const TensorIR& ir, const Inputs& inputs, const ComputeOp* epilogue_op) {

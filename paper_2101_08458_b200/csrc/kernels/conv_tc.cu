@@ -429,7 +429,7 @@ Status plan_problem(const Problem& pb_in, tzc_plan* plan) {
     const bool s2d = needs_k7(pb_in) && s2d_eligible(pb_in);
     const Problem q = s2d ? s2d_problem(pb_in) : pb_in;
     WsPlan w;
-    if ((s2d || (!needs_k7(pb_in) && g_ws_enabled)) && ws_plan(q, s2d && !pb_in.f16, &w)) {
+    if ((s2d || (!needs_k7(pb_in) && g_ws_enabled && pb_in.forced_splits < 2)) && ws_plan(q, s2d && !pb_in.f16, &w)) {
       plan->bm = 128 * w.mt;  // rows per work unit
       plan->bn = w.bn;
       plan->bk_bytes = w.kb;
@@ -470,7 +470,8 @@ Status plan_problem(const Problem& pb_in, tzc_plan* plan) {
   const int tiles_n = (pb.ngemm + bn - 1) / bn;
   const int num_kb = (int)(pb.taps * ((krow_bytes + kb - 1) / kb));
   const int tiles = tiles_m * tiles_n;
-  const WorkSplit wsplit = work_split(tiles, tiles_n, num_kb, sms, pb.ngemm % 16 == 0, g_forced_splits);
+  const WorkSplit wsplit =
+      work_split(tiles, tiles_n, num_kb, sms, pb.ngemm % 16 == 0, pb.forced_splits ? pb.forced_splits : g_forced_splits);
   const int splits = wsplit.splits;
   const int64_t red_m0 = (int64_t)(wsplit.full / tiles_n) * 128;
   const Entry* ent = find_entry(bn, kb, pb.f16, pb.a_mode, pb.b_kn);
@@ -922,7 +923,7 @@ Status run_problem(const Problem& pb, const void* a, const void* b, const void* 
   p.splits = plan.splits;
   {
     const WorkSplit wsplit = work_split(p.num_tiles, plan.tiles_n, p.num_kb, num_sms(), pb.ngemm % 16 == 0,
-                                        g_forced_splits);
+                                        pb.forced_splits ? pb.forced_splits : g_forced_splits);
     p.full_units = wsplit.full;
     p.red_m0 = (int32_t)((wsplit.full / plan.tiles_n) * 128);
     p.red_rows = (int32_t)(pb.m - p.red_m0);

@@ -33,6 +33,9 @@ struct Problem {
   int64_t w_stride_k = 0, w_stride_tap = 0;
   int b_kn = 0;    // fp16 matmul: B stored [K, N]
   tzc_out_layout out{};
+  // split-K factor requested by the op's schedule (split_reduction); 0 = the
+  // process-wide setting.  A forced split runs on the general kernel.
+  int forced_splits = 0;
 };
 
 Status plan_problem(const Problem& pb, tzc_plan* plan);

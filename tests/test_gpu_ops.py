@@ -186,3 +186,22 @@ def test_eval_tir_random_reference_schedules(cuda):
     for _ in range(6):
         sched = random_tcgen05_schedule(rng)
         assert np.array_equal(ops.eval_tir(text, "tcgen05_i8_m128n128k32", ins, schedule=sched), ref), sched
+
+
+def test_eval_tir_split_reduction_becomes_device_split_k(cuda):
+    """A schedule's split_reduction (rewriter.cpp:425-451) runs as the device
+    split-K (partials + wrap-add fix-up launch), bit-exact."""
+    from paper_2101_08458_b200 import device as D
+    text = matmul_tdsl(256, 256, 1024)
+    ins = Orc.random_inputs(decls(text), 23)
+    ref = Orc.matmul(ins["A"], ins["B"], ins["C"])
+    plain = "split x 128\nsplit y 128\nsplit k 32\nreorder x.o y.o k.o x.i y.i k.i\npragma x.i y.i k.i\n"
+    split = ("split x 128\nsplit y 128\nsplit k 32\nsplit_reduction k.o 4\n"
+             "reorder x.o y.o k.o.s k.o.r x.i y.i k.i\npragma x.i y.i k.i\n")
+    n0 = D.launch_count()
+    assert np.array_equal(ops.eval_tir(text, "tcgen05_i8_m128n128k32", ins, schedule=plain), ref)
+    n1 = D.launch_count()
+    assert np.array_equal(ops.eval_tir(text, "tcgen05_i8_m128n128k32", ins, schedule=split), ref)
+    n2 = D.launch_count()
+    assert n2 - n1 > n1 - n0  # the fix-up (fold) kernel launched
+    assert "C.partial" in ops.lower(text, split, "tcgen05_i8_m128n128k32")
