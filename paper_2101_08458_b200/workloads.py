@@ -158,3 +158,16 @@ def requant_scale(kg: int) -> float:
     import math
     sigma = 10880.0 * math.sqrt(kg)
     return 2.0 ** -round(math.log2(3 * sigma / 127.0))
+
+
+# The paper's Table-1 convolution bank (proj/src/workloads.cpp:123-142, table1_bank):
+# (name, in_c, in_hw, out_c, kernel, stride), lowered by conv2d_tdsl with the
+# reference's (lane_block, red_block) = (16, 4) channel blocking.
+TABLE1_BANK = [
+    ("conv01", 288, 35, 384, 3, 2), ("conv02", 160, 9, 224, 3, 1), ("conv03", 1056, 7, 192, 1, 1),
+    ("conv04", 80, 73, 192, 3, 1), ("conv05", 128, 16, 128, 3, 1), ("conv06", 192, 16, 192, 3, 1),
+    ("conv07", 256, 16, 256, 3, 1), ("conv08", 1024, 14, 512, 1, 1), ("conv09", 128, 16, 160, 3, 1),
+    ("conv10", 576, 14, 192, 1, 1), ("conv11", 96, 16, 128, 3, 1), ("conv12", 1024, 14, 256, 1, 1),
+    ("conv13", 576, 14, 128, 1, 1), ("conv14", 64, 29, 96, 3, 1), ("conv15", 64, 56, 128, 1, 2),
+    ("conv16", 608, 14, 192, 1, 1),
+]

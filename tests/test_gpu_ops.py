@@ -205,3 +205,19 @@ def test_eval_tir_split_reduction_becomes_device_split_k(cuda):
     n2 = D.launch_count()
     assert n2 - n1 > n1 - n0  # the fix-up (fold) kernel launched
     assert "C.partial" in ops.lower(text, split, "tcgen05_i8_m128n128k32")
+
+
+@pytest.mark.parametrize("shape", __import__("paper_2101_08458_b200.workloads", fromlist=["x"]).TABLE1_BANK,
+                         ids=lambda b: b[0])
+def test_table1_bank_on_device(cuda, shape):
+    """The paper's Table-1 bank (proj/src/workloads.cpp:123-142), exactly as the
+    reference lowers it (blocked layouts, accumulate-form seed), through
+    tzc_b200_run_op with tcgen05: bit-exact vs the oracle, and the fused requant."""
+    from paper_2101_08458_b200.workloads import conv2d_tdsl
+    _, c, hw, k, r, st = shape
+    text = conv2d_tdsl(c, hw, k, r, st)
+    ins = Orc.random_inputs(decls(text), 1000 + c)
+    ref = Orc.conv2d_blocked(ins["data"], ins["kernel"], st, ins["out"])
+    assert np.array_equal(ops.run_op(text, "tcgen05_i8_m128n64k32", ins), ref)
+    q = ops.run_op(text, "tcgen05_i8_m128n64k32", ins, epilogue=requant_tdsl(ref.shape, 2.0 ** -14, src="out"))
+    assert np.array_equal(q, Orc.requant_i8(ref, 2.0 ** -14))

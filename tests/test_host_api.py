@@ -11,7 +11,7 @@ import pytest
 from oracle.pyoracle import Ref
 from paper_2101_08458_b200 import ops
 from paper_2101_08458_b200._capi import TzcError
-from paper_2101_08458_b200.workloads import RESNET50_V15, conv2d_nhwc_tdsl, conv2d_tdsl, matmul_tdsl
+from paper_2101_08458_b200.workloads import RESNET50_V15, TABLE1_BANK, conv2d_nhwc_tdsl, conv2d_tdsl, matmul_tdsl
 
 needs_ref = pytest.mark.skipif(not Ref.available(), reason="oracle/_ref not built")
 
@@ -111,3 +111,15 @@ def test_unknown_intrinsic_and_no_kernel():
     with pytest.raises(TzcError) as e:  # the VNNI description has no sm_100a kernel
         ops.describe(matmul_tdsl(16, 16, 64), "vdot_16x4")
     assert e.value.kind == "NoFeasibleMapping"
+
+
+@needs_ref
+@pytest.mark.parametrize("shape", TABLE1_BANK, ids=[b[0] for b in TABLE1_BANK])
+def test_table1_bank_texts_and_plans(shape):
+    """The paper's Table-1 bank: our generator's op text is the reference's
+    (proj/src/workloads.cpp:123-142 through conv2d_tdsl), and each op has a
+    tcgen05 device plan (the blocked-conv family with the K5 adapters)."""
+    _, c, hw, k, r, st = shape
+    text = conv2d_tdsl(c, hw, k, r, st)
+    assert text == Ref.conv2d_tdsl(c, hw, k, r, st)
+    assert "plan conv_blocked u8i8" in ops.describe(text, "tcgen05_i8_m128n64k32")
