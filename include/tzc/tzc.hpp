@@ -272,7 +272,7 @@ InspectionReport inspect(const ComputeOp& op, const Intrinsic& intr);
 // How one op is executed by the sm_100a kernel (the analogue of the
 // reference's tensorize schedule + injected call).
 struct KernelPlan {
-  enum class Family : uint8_t { Matmul, ConvNHWC, ConvBlocked };
+  enum class Family : uint8_t { Matmul, ConvNHWC, ConvBlocked, ConvBlocked3D };
   Family family = Family::Matmul;
   bool f16 = false;
   // geometry in the kernel's GEMM view
@@ -284,6 +284,7 @@ struct KernelPlan {
   int64_t out_nb = 0, out_stride_m = 0, out_stride_blk = 0;
   std::string data, weight, out;  // op tensor names bound to a, b, d
   int64_t splits = 0;             // device split-K from the schedule's split_reduction (0 = planner's choice)
+  int64_t dp = 1, kd = 1, od = 1; // ConvBlocked3D: input depth, depth taps, output depth
   std::string describe() const;
 };
 struct TensorizedOp {

@@ -102,6 +102,7 @@ class Ref:
                 L.tzcref_tensor_text.argtypes = [C.c_char_p, _I64, C.c_char_p, _I64]
                 L.tzcref_matmul_tdsl.argtypes = [_I64, _I64, _I64, C.c_int, C.c_char_p, _I64]
                 L.tzcref_conv2d_tdsl.argtypes = [_I64] * 7 + [C.c_int, C.c_char_p, _I64]
+                L.tzcref_conv3d_tdsl.argtypes = [_I64] * 7 + [C.c_int, C.c_char_p, _I64]
                 L.tzcref_f64_to_f16_bits.argtypes = [C.c_double]
                 L.tzcref_f64_to_f16_bits.restype = C.c_uint16
                 L.tzcref_f16_bits_to_f64.argtypes = [C.c_uint16]
@@ -132,6 +133,12 @@ class Ref:
     def conv2d_tdsl(cls, in_c, in_hw, out_c, kernel, stride=1, lane_block=16, red_block=4,
                     fp16=False) -> str:
         return cls._text(cls.lib().tzcref_conv2d_tdsl, in_c, in_hw, out_c, kernel, stride,
+                         lane_block, red_block, int(fp16))
+
+    @classmethod
+    def conv3d_tdsl(cls, in_c, in_hw, out_c, kernel, stride=1, lane_block=16, red_block=4,
+                    fp16=False) -> str:
+        return cls._text(cls.lib().tzcref_conv3d_tdsl, in_c, in_hw, out_c, kernel, stride,
                          lane_block, red_block, int(fp16))
 
     @classmethod

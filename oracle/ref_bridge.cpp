@@ -281,6 +281,17 @@ int tzcref_conv2d_tdsl(int64_t in_c, int64_t in_hw, int64_t out_c, int64_t kerne
   TZCREF_CATCH
 }
 
+int tzcref_conv3d_tdsl(int64_t in_c, int64_t in_hw, int64_t out_c, int64_t kernel,
+                       int64_t stride, int64_t lane_block, int64_t red_block,
+                       int fp16, char* buf, int64_t buflen) {
+  TZCREF_TRY
+  ConvShape c{"conv3d", in_c, in_hw, out_c, kernel, stride};
+  return put_text(
+      conv3d_tdsl(c, lane_block, red_block, fp16 ? fp16_profile() : int8_profile()),
+      buf, buflen);
+  TZCREF_CATCH
+}
+
 uint16_t tzcref_f64_to_f16_bits(double x) { return f64_to_f16_bits(x); }
 double tzcref_f16_bits_to_f64(uint16_t b) { return f16_bits_to_f64(b); }
 

@@ -86,8 +86,12 @@ Deviation compare(const TensorValue& ref, const TensorValue& got, double rtol) {
 // ============================ planning ===================================
 std::string KernelPlan::describe() const {
   std::ostringstream os;
-  const char* fam = family == Family::Matmul ? "matmul" : family == Family::ConvNHWC ? "conv_nhwc" : "conv_blocked";
+  const char* fam = family == Family::Matmul        ? "matmul"
+                    : family == Family::ConvNHWC    ? "conv_nhwc"
+                    : family == Family::ConvBlocked ? "conv_blocked"
+                                                    : "conv3d_blocked";
   os << fam << (f16 ? " f16" : " u8i8") << " n=" << n << " hp=" << hp << " wp=" << wp << " c=" << c << " k=" << k
+     << (family == Family::ConvBlocked3D ? " dp=" + std::to_string(dp) + " kd=" + std::to_string(kd) : std::string())
      << " r=" << r << " s=" << s << " stride=" << stride << " m=" << m << (b_kn ? " b_kn" : "") << " out(nb=" << out_nb
      << ",sm=" << out_stride_m << ",sb=" << out_stride_blk << ")";
   return os.str();
@@ -276,7 +280,7 @@ KernelPlan plan_for(const ComputeOp& op, const Intrinsic& intr, const LoopMappin
       vb = t.var;
     }
     di = 1;
-  } else if (nd != 3) {
+  } else if (nd != 3 && !(blocked && nd == 5)) {
     throw InjectError("unsupported operand rank for a convolution");
   }
   auto spatial = [&](size_t i, std::string* vm, std::string* vt, int64_t* st) {
@@ -292,6 +296,54 @@ KernelPlan plan_for(const ComputeOp& op, const Intrinsic& intr, const LoopMappin
     }
     if (vm->empty()) throw InjectError("spatial index without an output-pixel loop");
   };
+  auto weight_dims = [&]() {
+    std::vector<std::string> wd;
+    for (const auto& e : B->args) {
+      auto [t, c] = terms_of(e);
+      if (t.size() != 1 || t[0].coeff != 1 || c != 0) throw InjectError("weight index is not a plain loop");
+      wd.push_back(t[0].var);
+    }
+    return wd;
+  };
+  if (nd == 5) {
+    // conv3d_tdsl (proj/src/workloads.cpp:94-121): data[co, d*st+rd, h*st+rh, w*st+rw, ci],
+    // kernel[ko, co, rd, rh, rw, ki, ci], out[ko, od, oh, ow, ki].  Executed as kd
+    // batched 2-D convs (one per depth tap) over the od output depth slices,
+    // accumulated through the int32 / fp32 C-seed (run_tensorized_packed).
+    std::string vd, vrd, vh3, vr3, vw3, vs3;
+    int64_t sd = 1, sh = 1, sw = 1;
+    spatial(1, &vd, &vrd, &sd);
+    spatial(2, &vh3, &vr3, &sh);
+    spatial(3, &vw3, &vs3, &sw);
+    if (sd != sh || sh != sw) throw InjectError("anisotropic strides are not supported");
+    if (Mv != std::vector<std::string>{vd, vh3, vw3}) throw InjectError("pixel loops must be fused in (od, oh, ow) order");
+    const Term tco = single(0), tci = single(4);
+    if (tco.var.empty() || tci.var != Kv || !in(taps, tco.var)) throw InjectError("blocked data must be [co, d, h, w, ci]");
+    const std::vector<std::string> wd = weight_dims();
+    if (vrd.empty() || vr3.empty() || vs3.empty() || wd.size() != 7 || wd[0] != Nv[0] || wd[1] != tco.var ||
+        wd[2] != vrd || wd[3] != vr3 || wd[4] != vs3 || wd[5] != Nv[1] || wd[6] != Kv)
+      throw InjectError("blocked 3-D kernel must be [ko, co, rd, rh, rw, ki, ci]");
+    p.family = KernelPlan::Family::ConvBlocked3D;
+    p.stride = sd;
+    p.kd = ext(op, vrd);
+    p.r = ext(op, vr3);
+    p.s = ext(op, vs3);
+    p.dp = td.shape[1];
+    p.hp = td.shape[2];
+    p.wp = td.shape[3];
+    p.od = ext(op, vd);
+    if ((p.dp - p.kd) / p.stride + 1 != p.od || (p.hp - p.r) / p.stride + 1 != ext(op, vh3) ||
+        (p.wp - p.s) / p.stride + 1 != ext(op, vw3))
+      throw InjectError("output window does not cover the input exactly");
+    p.n = p.od;
+    p.m = p.od * ext(op, vh3) * ext(op, vw3);
+    p.cb = ext(op, Kv);
+    p.kb = ext(op, Nv[1]);
+    p.c = ext(op, tco.var) * p.cb;
+    p.w_stride_k = p.kd * p.r * p.s * p.c;  // after the K5 adapter: [K, kd, R, S, C]
+    p.w_stride_tap = p.c;
+    return p;
+  }
   spatial(di, &vh, &vr, &sth);
   spatial(di + 1, &vw, &vs, &stw);
   if (sth != stw) throw InjectError("anisotropic strides are not supported");
@@ -442,7 +494,7 @@ struct DeviceBuf {
   void* p = nullptr;
   size_t bytes = 0;
 };
-thread_local DeviceBuf t_pool[8];
+thread_local DeviceBuf t_pool[9];
 
 void* pool(int slot, size_t bytes) {
   DeviceBuf& b = t_pool[slot];
@@ -659,6 +711,43 @@ void run_tensorized_packed(const TensorizedOp& t, const std::map<std::string, co
     if (!s1.ok()) throw DeviceError(s1.msg);
     a = ux;
     b = uw;
+  }
+  if (p.family == KernelPlan::Family::ConvBlocked3D) {
+    // one batched 2-D conv per depth tap rd over the od output slices (input
+    // slices rd, rd+st, ...), chained through the C-seed: ping-pong int32 /
+    // fp32 accumulators, the caller's epilogue on the last tap only.  The sum
+    // order per element is rd-major, exact for integers (wrap-add, F8).
+    const int eb = p.f16 ? 2 : 1;
+    void* ux = pool(4, xb);
+    void* uw = pool(5, wb);
+    Status s1 = unblock_data(dx, ux, (int)p.c, (int)(p.dp * p.hp), (int)p.wp, (int)p.cb, eb, st);
+    if (!s1.ok()) throw DeviceError(s1.msg);
+    s1 = unblock_kernel(dw, uw, (int)p.k, (int)p.c, (int)(p.kd * p.r), (int)p.s, (int)p.kb, (int)p.cb, eb, st);
+    if (!s1.ok()) throw DeviceError(s1.msg);
+    const size_t slice = (size_t)(p.hp * p.wp * p.c) * eb;
+    const size_t acc_bytes = (size_t)to.size() * 4;
+    void* acc[2] = {pool(6, acc_bytes), pool(7, acc_bytes)};
+    void* gathered = p.stride > 1 ? pool(8, slice * p.od) : nullptr;
+    const tzc_epilogue mid{p.f16 ? TZC_EP_F32 : TZC_EP_I32, 1.0f};
+    const void* seed = ds;
+    for (int64_t rd = 0; rd < p.kd; ++rd) {
+      const uint8_t* src = static_cast<const uint8_t*>(ux) + rd * slice;
+      const void* a3 = src;
+      if (p.stride > 1) {
+        cuda_ok(cudaMemcpy2DAsync(gathered, slice, src, slice * p.stride, slice, p.od, cudaMemcpyDeviceToDevice, st),
+                "depth-slice gather");
+        a3 = gathered;
+      }
+      const void* b3 = static_cast<const uint8_t*>(uw) + rd * (size_t)(p.r * p.s * p.c) * eb;
+      const bool last = rd == p.kd - 1;
+      void* o3 = last ? dout : acc[rd & 1];
+      const Status s = run_problem(problem(p.n), a3, b3, seed, o3, last ? e : mid, st);
+      if (!s.ok()) fail(s);
+      seed = o3;
+    }
+    cuda_ok(cudaMemcpyAsync(host_out, dout, (size_t)out_bytes, cudaMemcpyDeviceToHost, st), "D2H output");
+    cuda_ok(cudaStreamSynchronize(st), "tensorized op");
+    return;
   }
   const Status s = run_problem(problem(p.family == KernelPlan::Family::Matmul ? p.m : p.n), a, b, ds, dout, e, st);
   if (!s.ok()) fail(s);

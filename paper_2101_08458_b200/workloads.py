@@ -49,6 +49,23 @@ def conv2d_tdsl(in_c, in_hw, out_c, kernel, stride=1, lane_block=16, red_block=4
             f"out[ko, oh, ow, ki] += cast<{a}>({data}) * cast<{a}>(kernel[ko, co, r, s, ki, ci])\n")
 
 
+def conv3d_tdsl(in_c, in_hw, out_c, kernel, stride=1, lane_block=16, red_block=4, fp16=False) -> str:
+    """The reference's conv3d_tdsl (proj/src/workloads.cpp:94-121): channel-blocked
+    valid 3-D conv, data [C/rb, D, H, W, rb], kernel [K/lb, C/rb, kd, kh, kw, lb, rb]."""
+    d, w, a = _dt(fp16)
+    co, ko = in_c // red_block, out_c // lane_block
+    o = (in_hw - kernel) // stride + 1
+    x = (f"data[co, {_strided('od', stride, 'rd')}, {_strided('oh', stride, 'rh')}, "
+         f"{_strided('ow', stride, 'rw')}, ci]")
+    return (f"tensor data : {d} [{co}, {in_hw}, {in_hw}, {in_hw}, {red_block}] input\n"
+            f"tensor kernel : {w} [{ko}, {co}, {kernel}, {kernel}, {kernel}, {lane_block}, {red_block}] input\n"
+            f"tensor out : {a} [{ko}, {o}, {o}, {o}, {lane_block}] output\n"
+            f"loop ko : dp {ko}\nloop od : dp {o}\nloop oh : dp {o}\nloop ow : dp {o}\nloop ki : dp {lane_block}\n"
+            f"loop co : red {co}\nloop rd : red {kernel}\nloop rh : red {kernel}\nloop rw : red {kernel}\n"
+            f"loop ci : red {red_block}\n"
+            f"out[ko, od, oh, ow, ki] += cast<{a}>({x}) * cast<{a}>(kernel[ko, co, rd, rh, rw, ki, ci])\n")
+
+
 def conv2d_nhwc_tdsl(n, hp, wp, c, k, r, s, stride=1, fp16=False) -> str:
     d, w, a = _dt(fp16)
     oh, ow = (hp - r) // stride + 1, (wp - s) // stride + 1

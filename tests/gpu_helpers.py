@@ -34,3 +34,16 @@ def rel_dev(ref: np.ndarray, got: np.ndarray) -> float:
     ref = ref.astype(np.float64)
     got = got.astype(np.float64)
     return float(np.max(np.abs(ref - got) / np.maximum(np.abs(ref), 1.0))) if ref.size else 0.0
+
+
+def read_tnsr(path):
+    """numpy view of a TNSR container (proj/src/vm.cpp:686-822 layout)."""
+    import struct
+
+    import numpy as np
+    raw = open(path, "rb").read()
+    assert raw[:4] == b"TNSR" and raw[4] == 1
+    dt = [np.uint8, np.int8, np.uint16, np.int16, np.uint32, np.int32, np.float16, np.float32][raw[5]]
+    rank = raw[6]
+    shape = struct.unpack("<%dQ" % rank, raw[7:7 + 8 * rank])
+    return np.frombuffer(raw[7 + 8 * rank:], dtype=dt).reshape(shape)

@@ -221,3 +221,18 @@ def test_table1_bank_on_device(cuda, shape):
     assert np.array_equal(ops.run_op(text, "tcgen05_i8_m128n64k32", ins), ref)
     q = ops.run_op(text, "tcgen05_i8_m128n64k32", ins, epilogue=requant_tdsl(ref.shape, 2.0 ** -14, src="out"))
     assert np.array_equal(q, Orc.requant_i8(ref, 2.0 ** -14))
+
+
+@pytest.mark.parametrize("name", ["conv3d_i8", "conv3d_s2_i8"])
+def test_conv3d_run_op_with_requant(cuda, name):
+    """conv3d_tdsl through tzc_b200_run_op (depth-tap decomposition chained through
+    the int32 C-seed): the reference's own output (saved by make_tnsr.py) bit for
+    bit, and the fused requant on the last tap."""
+    from tests.gpu_helpers import read_tnsr
+    d = os.path.join(GOLD, "tnsr", name)
+    text = open(os.path.join(d, "op.tdsl")).read()
+    ins = {n: read_tnsr(os.path.join(d, n + ".tnsr")) for n in ("data", "kernel", "out")}
+    want = read_tnsr(os.path.join(d, "expect.tnsr"))
+    assert np.array_equal(ops.run_op(text, "tcgen05_i8_m128n64k32", ins), want)
+    q = ops.run_op(text, "tcgen05_i8_m128n64k32", ins, epilogue=requant_tdsl(want.shape, 2.0 ** -13, src="out"))
+    assert np.array_equal(q, Orc.requant_i8(want, 2.0 ** -13))

@@ -11,7 +11,7 @@ import pytest
 from oracle.pyoracle import Ref
 from paper_2101_08458_b200 import ops
 from paper_2101_08458_b200._capi import TzcError
-from paper_2101_08458_b200.workloads import RESNET50_V15, TABLE1_BANK, conv2d_nhwc_tdsl, conv2d_tdsl, matmul_tdsl
+from paper_2101_08458_b200.workloads import RESNET50_V15, TABLE1_BANK, conv2d_nhwc_tdsl, conv2d_tdsl, conv3d_tdsl, matmul_tdsl
 
 needs_ref = pytest.mark.skipif(not Ref.available(), reason="oracle/_ref not built")
 
@@ -123,3 +123,17 @@ def test_table1_bank_texts_and_plans(shape):
     text = conv2d_tdsl(c, hw, k, r, st)
     assert text == Ref.conv2d_tdsl(c, hw, k, r, st)
     assert "plan conv_blocked u8i8" in ops.describe(text, "tcgen05_i8_m128n64k32")
+
+
+@needs_ref
+@pytest.mark.parametrize("args", [(16, 8, 32, 3, 1, False), (16, 9, 32, 3, 2, False), (16, 7, 16, 3, 1, True),
+                                  (64, 16, 64, 3, 1, False), (64, 17, 128, 3, 2, False)])
+def test_conv3d_texts_and_plans(args):
+    """conv3d_tdsl (proj/src/workloads.cpp:94-121): same text as the reference's
+    generator, and a device plan (depth-tap decomposition, conv3d_blocked)."""
+    c, hw, k, r, st, f16 = args
+    text = conv3d_tdsl(c, hw, k, r, st, fp16=f16)
+    assert text == Ref.conv3d_tdsl(c, hw, k, r, st, fp16=f16)
+    intr = "tcgen05_f16_m128n64k16" if f16 else "tcgen05_i8_m128n64k32"
+    assert "plan conv3d_blocked" in ops.describe(text, intr)
+    assert ops.lower(text, None, intr).count(intr + "(dst = ") == 1
