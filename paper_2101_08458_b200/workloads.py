@@ -188,3 +188,12 @@ TABLE1_BANK = [
     ("conv13", 576, 14, 128, 1, 1), ("conv14", 64, 29, 96, 3, 1), ("conv15", 64, 56, 128, 1, 2),
     ("conv16", 608, 14, 192, 1, 1),
 ]
+
+# The resnet18-3d bank (proj/src/workloads.cpp:149-162, resnet18_3d_bank), lowered
+# by conv3d_tdsl with (16, 4) blocking: (name, in_c, in_hw, out_c, kernel, stride).
+RESNET18_3D_BANK = [
+    ("block2_conv", 64, 56, 64, 3, 1), ("block3_down", 64, 56, 128, 3, 2), ("block3_conv", 128, 28, 128, 3, 1),
+    ("block3_skip", 64, 56, 128, 1, 2), ("block4_down", 128, 28, 256, 3, 2), ("block4_conv", 256, 14, 256, 3, 1),
+    ("block4_skip", 128, 28, 256, 1, 2), ("block5_down", 256, 14, 512, 3, 2), ("block5_conv", 512, 7, 512, 3, 1),
+    ("block5_skip", 256, 14, 512, 1, 2),
+]

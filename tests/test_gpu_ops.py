@@ -236,3 +236,26 @@ def test_conv3d_run_op_with_requant(cuda, name):
     assert np.array_equal(ops.run_op(text, "tcgen05_i8_m128n64k32", ins), want)
     q = ops.run_op(text, "tcgen05_i8_m128n64k32", ins, epilogue=requant_tdsl(want.shape, 2.0 ** -13, src="out"))
     assert np.array_equal(q, Orc.requant_i8(want, 2.0 ** -13))
+
+
+@pytest.mark.parametrize("shape", __import__("paper_2101_08458_b200.workloads", fromlist=["x"]).RESNET18_3D_BANK,
+                         ids=lambda b: b[0])
+def test_resnet18_3d_bank_on_device(cuda, shape):
+    """The resnet18-3d bank at full size through tzc_b200_run_op; 64 sampled
+    output elements recomputed exactly (int64 sums wrapped to int32) — the full
+    op is hours of reference-VM time."""
+    from paper_2101_08458_b200.workloads import conv3d_tdsl
+    _, c, hw, k, r, st = shape
+    text = conv3d_tdsl(c, hw, k, r, st)
+    dec = decls(text)
+    data = Orc.random_tensor("u8", dec[0][3], 100 + c)
+    kern = Orc.random_tensor("i8", dec[1][3], 200 + k)
+    out = ops.run_op(text, "tcgen05_i8_m128n64k32", {"data": data, "kernel": kern})
+    rng = np.random.default_rng(c * k)
+    ko_n, o = out.shape[0], out.shape[1]
+    for _ in range(64):
+        ko, od, oh, ow, ki = (int(rng.integers(0, n)) for n in (ko_n, o, o, o, 16))
+        x = data[:, od * st:od * st + r, oh * st:oh * st + r, ow * st:ow * st + r, :].astype(np.int64)
+        w = kern[ko, :, :, :, :, ki, :].astype(np.int64)
+        want = np.int64((x * w).sum()).astype(np.int32)
+        assert out[ko, od, oh, ow, ki] == want, (ko, od, oh, ow, ki)
