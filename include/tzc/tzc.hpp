@@ -428,6 +428,10 @@ TensorValue run_tensorized(const TensorizedOp& t, const Inputs& inputs, const Co
 // description run (on the B200); anything else throws InjectError — there is
 // no CPU interpreter behind this entry point.
 TensorValue eval_tir(const TensorIR& ir, const Inputs& inputs, const ComputeOp* epilogue_op = nullptr);
+// Measured-time plan search for a tensorized matmul / NHWC conv on the B200
+// (tzc_b200_tune_*): one "candidate <i> <options> <us> us" line per candidate
+// plan and a "best" line; the winner is installed for that device problem.
+std::string tune_tensorized(const TensorizedOp& t, const Inputs& inputs, int reps = 10);
 // The device plan eval_tir executes for `ir` (InjectError as above).
 TensorizedOp device_plan(const TensorIR& ir);
 

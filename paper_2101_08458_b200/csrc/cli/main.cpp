@@ -27,6 +27,7 @@ const char* kUsage =
     "  tensorize OP.tdsl --intrinsic X [--schedule-out PATH]\n"
     "  run       OP.tdsl --intrinsic X [--schedule PATH] [--input name=PATH]... [--seed N]\n"
     "            [--epilogue OP.tdsl] [--output PATH] [--format text|structured]\n"
+    "  tune      OP.tdsl --intrinsic X [--reps N] [--input name=PATH]... [--seed N]\n"
     "  verify    OP.tdsl --intrinsic X --expect PATH [--input name=PATH]... [--seed N]\n"
     "            [--epilogue OP.tdsl] [--rtol R] [--format text|structured]\n";
 
@@ -40,6 +41,7 @@ struct Args {
   uint64_t seed = 0;
   double rtol = 0.0;
   bool rtol_set = false;
+  int reps = 10;
 };
 
 Args parse_args(int argc, char** argv) {
@@ -62,6 +64,7 @@ Args parse_args(int argc, char** argv) {
     else if (k == "--format") a.format = val();
     else if (k == "--seed") a.seed = std::strtoull(val().c_str(), nullptr, 10);
     else if (k == "--rtol") a.rtol = std::atof(val().c_str()), a.rtol_set = true;
+    else if (k == "--reps") a.reps = std::atoi(val().c_str());
     else if (!k.empty() && k[0] == '-') throw Usage("unknown option " + k);
     else if (a.op_path.empty()) a.op_path = k;
     else throw Usage("unexpected argument " + k);
@@ -218,6 +221,15 @@ int cmd_verify(const Args& a, std::ostream& out) {
   return pass ? 0 : 1;
 }
 
+// The device analogue of `tzc tune --target gpu` (proj/src/cli.cpp tune
+// subcommand): candidate plans timed with CUDA events, the log printed.
+int cmd_tune(const Args& a, std::ostream& out) {
+  const tzc::ComputeOp op = load_op(a);
+  const tzc::TensorizedOp t = tzc::tensorize(op, need_intrinsic(a));
+  out << "plan " << t.plan.describe() << "\n" << tzc::tune_tensorized(t, gather_inputs(a, op), a.reps);
+  return 0;
+}
+
 bool domain_failure(const std::string& kind) {
   return kind == "NoFeasibleMapping" || kind == "DivisibilityError" || kind == "PadUnsupported" ||
          kind == "InjectError" || kind == "DeviceError";
@@ -236,6 +248,7 @@ int main(int argc, char** argv) {
     if (a.cmd == "tensorize") return cmd_tensorize(a, std::cout);
     if (a.cmd == "run") return cmd_run(a, std::cout);
     if (a.cmd == "verify") return cmd_verify(a, std::cout);
+    if (a.cmd == "tune") return cmd_tune(a, std::cout);
     throw Usage("unknown command '" + a.cmd + "'");
   } catch (const Usage& e) {
     std::cerr << "error: " << e.what() << "\n" << kUsage;

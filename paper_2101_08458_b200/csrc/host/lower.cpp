@@ -755,12 +755,13 @@ void run_tensorized_packed(const TensorizedOp& t, const std::map<std::string, co
   cuda_ok(cudaStreamSynchronize(st), "tensorized op");
 }
 
-TensorValue run_tensorized(const TensorizedOp& t, const Inputs& inputs, const ComputeOp* epilogue_op) {
-  // pack TensorValues at their declared widths, run, unpack
+namespace {
+
+// TensorValues packed at their declared element widths (the C ABI's buffers).
+std::map<std::string, std::vector<uint8_t>> pack_inputs(const ComputeOp& op, const Inputs& inputs) {
   std::map<std::string, std::vector<uint8_t>> packed;
-  std::map<std::string, const void*> ptrs;
   for (const auto& [name, v] : inputs) {
-    const TensorDecl* d = t.op.find_tensor(name);
+    const TensorDecl* d = op.find_tensor(name);
     if (!d) throw MissingInput("no tensor named '" + name + "'");
     if (v.dtype != d->dtype || v.shape != d->shape) throw ShapeError("input '" + name + "' does not match its declaration");
     std::vector<uint8_t> buf(v.size() * elem_bytes(d->dtype));
@@ -777,8 +778,77 @@ TensorValue run_tensorized(const TensorizedOp& t, const Inputs& inputs, const Co
       }
     }
     packed[name] = std::move(buf);
-    ptrs[name] = packed[name].data();
   }
+  return packed;
+}
+
+}  // namespace
+
+std::string tune_tensorized(const TensorizedOp& t, const Inputs& inputs, int reps) {
+  using namespace tzcb200;
+  const KernelPlan& p = t.plan;
+  if (p.family != KernelPlan::Family::Matmul && p.family != KernelPlan::Family::ConvNHWC)
+    throw InjectError("tune times matmul / NHWC-conv plans; blocked layouts run those after the K5 adapters");
+  auto packed = pack_inputs(t.op, inputs);
+  auto dev = [&](int slot, const std::string& name) -> void* {
+    auto it = packed.find(name);
+    if (it == packed.end()) return nullptr;
+    void* d = pool(slot, it->second.size());
+    cuda_ok(cudaMemcpy(d, it->second.data(), it->second.size(), cudaMemcpyHostToDevice), "H2D");
+    return d;
+  };
+  void* dx = dev(0, p.data);
+  void* dw = dev(1, p.weight);
+  if (!dx || !dw) throw MissingInput("tune needs the data and weight tensors");
+  void* ds = t.op.update ? dev(2, t.op.out) : nullptr;
+  const TensorDecl& to = t.op.output();
+  void* dout = pool(3, (size_t)to.size() * elem_bytes(to.dtype));
+  tzc_out_layout ol{};
+  ol.nb = (int32_t)p.out_nb;
+  ol.stride_m = p.out_stride_m;
+  ol.stride_blk = p.out_stride_blk;
+  const tzc_epilogue e{p.f16 ? TZC_EP_F32 : TZC_EP_I32, 1.0f};
+  char log[1 << 14];
+  log[0] = 0;
+  int rc;
+  if (p.family == KernelPlan::Family::Matmul) {
+    tzc_gemm_desc g{};
+    g.profile = p.f16 ? TZC_PROFILE_F16 : TZC_PROFILE_U8I8;
+    g.m = (int32_t)p.m;
+    g.n = (int32_t)p.k;
+    g.k = (int32_t)p.c;
+    g.b_kn = p.b_kn ? 1 : 0;
+    g.out = ol;
+    rc = tzc_b200_tune_gemm(&g, dx, dw, ds, dout, &e, reps, 1, log, sizeof log, nullptr);
+  } else {
+    tzc_conv_desc c{};
+    c.profile = p.f16 ? TZC_PROFILE_F16 : TZC_PROFILE_U8I8;
+    c.n = (int32_t)p.n;
+    c.hp = (int32_t)p.hp;
+    c.wp = (int32_t)p.wp;
+    c.c = (int32_t)p.c;
+    c.k = (int32_t)p.k;
+    c.r = (int32_t)p.r;
+    c.s = (int32_t)p.s;
+    c.stride = (int32_t)p.stride;
+    c.w_stride_k = p.w_stride_k;
+    c.w_stride_tap = p.w_stride_tap;
+    c.out = ol;
+    rc = tzc_b200_tune_conv(&c, dx, dw, ds, dout, &e, reps, 1, log, sizeof log, nullptr);
+  }
+  if (rc < 0) {
+    const std::string msg = tzc_b200_last_error();
+    if (rc == TZC_E_DEVICE) throw DeviceError(msg);
+    throw InjectError(msg);
+  }
+  return log;
+}
+
+TensorValue run_tensorized(const TensorizedOp& t, const Inputs& inputs, const ComputeOp* epilogue_op) {
+  // pack TensorValues at their declared widths, run, unpack
+  const std::map<std::string, std::vector<uint8_t>> packed = pack_inputs(t.op, inputs);
+  std::map<std::string, const void*> ptrs;
+  for (const auto& [name, buf] : packed) ptrs[name] = buf.data();
   const Epi ep = epilogue_of(t.op, epilogue_op);
   const std::vector<int64_t>& shape = t.op.output().shape;
   TensorValue out = TensorValue::zeros(ep.out_dtype, shape);

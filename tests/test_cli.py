@@ -85,3 +85,13 @@ def test_cli_exit_codes(tmp_path):
     shutil.copy(mm, tmp_path / "mm.tdsl")
     rc, _, err = cli("run", str(tmp_path / "mm.tdsl"), "--intrinsic", "vdot_16x4")
     assert rc == 1 and "InjectError" in err
+
+
+@needs_cli
+def test_cli_tune_without_device_is_a_domain_failure():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("a device is present (tests/test_gpu_cli.py covers tune)")
+    op = os.path.join(ROOT, "tests", "golden", "tnsr", "mm_i8", "op.tdsl")
+    rc, out, err = cli("tune", op, "--intrinsic", "tcgen05_i8_m128n128k32")
+    assert rc == 1 and out.startswith("plan matmul u8i8") and "DeviceError" in err

@@ -53,3 +53,15 @@ def test_cli_run_output_and_failing_verify(cuda, name, tmp_path):
     bad.write_bytes(bytes(raw))
     rc, out, _ = cli("verify", *args, "--expect", str(bad), "--format", "structured")
     assert rc == 1 and '"pass": false' in out and '"mismatches": 1' in out
+
+
+@pytest.mark.parametrize("name", ["mm_i8", "conv_nhwc_i8"])
+def test_cli_tune(cuda, name):
+    """`tzc-b200 tune`: 17 candidate plans timed on the device, the winner reported."""
+    d, args = case_args(name)
+    rc, out, err = cli("tune", *args[:3], "--reps", "3")
+    assert rc == 0, err
+    lines = out.strip().splitlines()
+    assert lines[0].startswith("plan ")
+    assert sum(ln.startswith("candidate ") for ln in lines) == 17
+    assert lines[-1].startswith("best ")
