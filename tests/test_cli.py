@@ -95,3 +95,17 @@ def test_cli_tune_without_device_is_a_domain_failure():
     op = os.path.join(ROOT, "tests", "golden", "tnsr", "mm_i8", "op.tdsl")
     rc, out, err = cli("tune", op, "--intrinsic", "tcgen05_i8_m128n128k32")
     assert rc == 1 and out.startswith("plan matmul u8i8") and "DeviceError" in err
+
+
+def test_reference_style_cpp_caller(tmp_path):
+    """C++ drop-in: a caller written against the reference's header paths and names
+    builds against libtzc_b200.so and prints acceptance criterion 2's golden IR."""
+    from tests.test_tensor_ir import C2_OP, C2_SCHED
+    exe = str(tmp_path / "chain")
+    lib_dir = os.path.join(ROOT, "paper_2101_08458_b200")
+    subprocess.run(["g++", "-std=c++17", "-O1", "-I", os.path.join(ROOT, "include"),
+                    os.path.join(ROOT, "tests", "cpp", "chain.cpp"), "-o", exe, "-L", lib_dir, "-ltzc_b200",
+                    f"-Wl,-rpath,{lib_dir}"], check=True, timeout=300)
+    p = subprocess.run([exe, "vdot_16x4", C2_SCHED], input=C2_OP, capture_output=True, text=True, timeout=60)
+    assert p.returncode == 0, p.stderr
+    assert p.stdout == open(os.path.join(ROOT, "tests", "golden", "conv_ir_c2_vdot_16x4.txt")).read()
