@@ -429,6 +429,14 @@ def run_ours(args, rank, world, local):
     with torch.cuda.graph(graph_l, stream=stream):
         suite(True)
     torch.cuda.synchronize()
+    # parity gate: one replay of the timed graph, checked against the oracle
+    for b in bufs:
+        b["out"].fill_(0x5A if b["out"].dtype == torch.int8 else 0)
+    torch.cuda.synchronize()  # the fills run on the default stream, the replay on `stream`
+    with torch.cuda.stream(stream):
+        graph.replay()
+    torch.cuda.synchronize()
+    parity = parity_gate(torch, bufs, args.profile)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 
     def step():
@@ -515,6 +523,7 @@ def run_ours(args, rank, world, local):
                    **({"tuned_plans": tuned} if args.tune else {})},
         "pct_of_spec_peak": round(100.0 * value / (spec * world), 2),
         "gpu_launches": launches_per_step * args.steps,
+        "parity": parity,
         "clocks": clk.summary(),
     }
     kern_ms = sum(statistics.median(v) for v in per_layer)  # per-layer event sum (graph B)
@@ -567,6 +576,46 @@ def run_ours(args, rank, world, local):
                         for r in layer_rows]
     if rank == 0:
         print(json.dumps(result))
+
+
+def parity_gate(torch, bufs, profile):
+    """Before any timing: the timed graph has been replayed once; check whole
+    images of every layer's output against the CPU oracle (the checker only,
+    outside every timed region).  int8: bit-exact requantized images (first
+    and last image of the shard, i.e. the first and the last work unit);
+    fp16: the reference's compare() metric <= 1e-3.  Raises on mismatch so no
+    value is ever printed for a wrong result.  Semantics: eval_reference,
+    /root/reference/proj/src/vm.cpp:444-508 (+ the requant op)."""
+    import numpy as np
+
+    from oracle.pyoracle import Orc
+    worst = 0.0
+    for b in bufs:
+        L = b["layer"]
+        nb = b["x"].shape[0]
+        for img in sorted({0, nb - 1}):
+            x = b["x"][img:img + 1].cpu().numpy()
+            w = b["w"].cpu().numpy()
+            got = b["out"][img:img + 1].cpu()
+            if profile == "f16":
+                ref = Orc.conv2d_nhwc(x.view(np.uint16), w.view(np.uint16), L.stride, fp16=True)
+                g = got.float().numpy().astype(np.float64)
+                rel = float(np.max(np.abs(g - ref) / np.maximum(np.abs(ref), 1.0)))
+                worst = max(worst, rel)
+                if rel > 1e-3:
+                    raise SystemExit(f"parity gate: {L.name} image {img}: max rel {rel:.3g} > 1e-3")
+            else:
+                want = Orc.requant_i8(Orc.conv2d_nhwc(x, w, L.stride), b["scale"])
+                if not np.array_equal(got.numpy(), want):
+                    bad = int((got.numpy() != want).sum())
+                    raise SystemExit(f"parity gate: {L.name} image {img}: {bad} int8 outputs differ from the oracle")
+    res = {"layers": len(bufs), "images_per_layer": 2, "checked_after": "one replay of the timed graph"}
+    if profile == "f16":
+        res["max_rel"] = worst
+        res["within_1e-3"] = True
+    else:
+        res["bitexact"] = True
+    return res
 
 
 def plan_of(D, b):
@@ -640,6 +689,11 @@ def run_e2e(args, torch, D, bufs, stream, ops_step, world, dist):
     for _ in range(max(1, args.warmup)):
         step()
     torch.cuda.synchronize()
+    # the e2e outputs (host buffers written by run_op) must equal the device
+    # path's outputs for the same inputs, byte for byte, on every layer
+    for (text, instr, ins, ep, out, _), b in zip(work, bufs):
+        if not (out == b["out"].cpu().numpy()).all():
+            raise SystemExit(f"e2e parity: {b['layer'].name}: run_op output differs from the device path")
     if world > 1:
         dist.barrier()
     steps = max(3, min(args.steps, 10))
@@ -652,6 +706,7 @@ def run_e2e(args, torch, D, bufs, stream, ops_step, world, dist):
             "ms_per_step": round(ms, 3), "steps": steps,
             "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
             "host_threads": args.e2e_threads,
+            "outputs_checked": "every layer's run_op output == the device-path output (bit-exact, after warm-up)",
             "path": "tzc_b200_run_op (op text + tcgen05 instruction + pinned host buffers + fused requant op), "
                     "synchronous per call, layers issued from host_threads threads; host wall clock, max over ranks"}
 

@@ -132,60 +132,9 @@ using namespace tzcb200;
 
 namespace {
 
-int set_option_raw(const std::string& n, int64_t value);
-
-// Process-wide option values (the defaults of conv_tc.cu) and per-problem
-// overrides installed by the measured tuner (tzc_b200_tune_*): a launch whose
-// descriptor has an entry runs with those options, then the process values
-// come back.  Options change the kernel plan only, never the results.
-std::mutex g_opt_mu;
-std::map<std::string, int64_t> g_opt_now = {
-    {"splits", 0},      {"shifted_window", 1}, {"ws_epi_groups", 1}, {"tail_split", 0}, {"split_min_kb", 1 << 20},
-    {"pingpong_kb", 2}, {"ws_mt", 0},          {"ws_1x1_k", 64},     {"ws_1x1", 0},     {"bn", 0},
-    {"tma_store_k", 64}, {"pair_min_kb", 16},  {"pair", 0},          {"st256", 1},      {"l2_hints", 1},
-    {"tma_store", 0}};
-using Overrides = std::vector<std::pair<std::string, int64_t>>;
-std::map<std::string, Overrides> g_problem_opts;
-
 template <typename D>
 std::string key_of(const D& d, char kind) {
   return std::string(1, kind) + std::string(reinterpret_cast<const char*>(&d), sizeof(D));
-}
-
-class ScopedOptions {
- public:
-  explicit ScopedOptions(const Overrides& o) : lk_(g_opt_mu, std::defer_lock), o_(o) {
-    if (o_.empty()) return;
-    lk_.lock();
-    for (const auto& [n, v] : o_) set_option_raw(n, v);
-  }
-  ~ScopedOptions() {
-    for (const auto& [n, v] : o_) set_option_raw(n, g_opt_now[n]);
-  }
-
- private:
-  std::unique_lock<std::mutex> lk_;
-  Overrides o_;
-};
-
-Overrides overrides_for(const std::string& key) {
-  std::lock_guard<std::mutex> lk(g_opt_mu);
-  auto it = g_problem_opts.find(key);
-  return it == g_problem_opts.end() ? Overrides{} : it->second;
-}
-
-Overrides parse_overrides(const std::string& spec) {
-  Overrides o;
-  size_t i = 0;
-  while (i < spec.size()) {
-    size_t j = spec.find(';', i);
-    if (j == std::string::npos) j = spec.size();
-    const std::string kv = spec.substr(i, j - i);
-    const size_t eq = kv.find('=');
-    if (eq != std::string::npos) o.emplace_back(kv.substr(0, eq), std::stoll(kv.substr(eq + 1)));
-    i = j + 1;
-  }
-  return o;
 }
 
 int run_conv(const tzc_conv_desc* d, int profile, const void* x, const void* w, const void* seed, void* out,
@@ -199,8 +148,7 @@ int run_conv(const tzc_conv_desc* d, int profile, const void* x, const void* w, 
   if (st.ok()) st = check_ptr(seed, "c_seed", true, false);
   if (st.ok()) st = check_ptr(out, "out", false, false);
   if (!st.ok()) return report(st);
-  ScopedOptions so(overrides_for(key_of(*d, 'c')));
-  return report(run_problem(pb, x, w, seed, out, *ep, static_cast<cudaStream_t>(stream)));
+  return report(run_problem(pb, options_for(key_of(*d, 'c')), x, w, seed, out, *ep, static_cast<cudaStream_t>(stream)));
 }
 
 int run_gemm(const tzc_gemm_desc* d, int profile, const void* a, const void* b, const void* seed, void* out,
@@ -214,8 +162,7 @@ int run_gemm(const tzc_gemm_desc* d, int profile, const void* a, const void* b, 
   if (st.ok()) st = check_ptr(seed, "c_seed", true, false);
   if (st.ok()) st = check_ptr(out, "out", false, false);
   if (!st.ok()) return report(st);
-  ScopedOptions so(overrides_for(key_of(*d, 'g')));
-  return report(run_problem(pb, a, b, seed, out, *ep, static_cast<cudaStream_t>(stream)));
+  return report(run_problem(pb, options_for(key_of(*d, 'g')), a, b, seed, out, *ep, static_cast<cudaStream_t>(stream)));
 }
 
 }  // namespace
@@ -255,7 +202,7 @@ int tzc_b200_plan_conv(const tzc_conv_desc* d, tzc_plan* plan) {
   if (!d || !plan) return report(Status(TZC_E_MISSING_INPUT, "NULL argument"));
   Problem pb;
   Status st = problem_from_conv(*d, &pb);
-  if (st.ok()) st = plan_problem(pb, plan);
+  if (st.ok()) st = plan_problem(pb, options_for(key_of(*d, 'c')), plan);
   return report(st);
   TZC_GUARD_END
 }
@@ -265,100 +212,23 @@ int tzc_b200_plan_gemm(const tzc_gemm_desc* d, tzc_plan* plan) {
   if (!d || !plan) return report(Status(TZC_E_MISSING_INPUT, "NULL argument"));
   Problem pb;
   Status st = problem_from_gemm(*d, &pb);
-  if (st.ok()) st = plan_problem(pb, plan);
+  if (st.ok()) st = plan_problem(pb, options_for(key_of(*d, 'g')), plan);
   return report(st);
   TZC_GUARD_END
 }
 
 }  // extern "C"
 
-namespace {
-
-int set_option_raw(const std::string& n, int64_t value) {
-  if (n == "splits") {
-    if (value < 0) return report(Status(TZC_E_SHAPE, "splits must be >= 0"));
-    set_forced_splits((int)value);
-    return TZC_OK;
-  }
-  if (n == "shifted_window") {
-    set_ws_enabled(value ? 1 : 0);
-    return TZC_OK;
-  }
-  if (n == "ws_epi_groups") {
-    set_ws_epi_groups((int)value);
-    return TZC_OK;
-  }
-  if (n == "tail_split") {
-    set_tail_split((int)value);
-    return TZC_OK;
-  }
-  if (n == "split_min_kb") {
-    set_split_min_kb((int)value);
-    return TZC_OK;
-  }
-  if (n == "pingpong_kb") {
-    set_pingpong_kb((int)value);
-    return TZC_OK;
-  }
-  if (n == "ws_mt") {
-    set_ws_mt((int)value);
-    return TZC_OK;
-  }
-  if (n == "ws_1x1_k") {
-    set_ws_1x1_k((int)value);
-    return TZC_OK;
-  }
-  if (n == "ws_1x1") {
-    set_ws_1x1((int)value);
-    return TZC_OK;
-  }
-  if (n == "bn") {
-    set_forced_bn((int)value);
-    return TZC_OK;
-  }
-  if (n == "tma_store_k") {
-    set_tma_store_k((int)value);
-    return TZC_OK;
-  }
-  if (n == "pair_min_kb") {
-    set_pair_min_kb((int)value);
-    return TZC_OK;
-  }
-  if (n == "pair") {
-    set_pair((int)value);
-    return TZC_OK;
-  }
-  if (n == "st256") {
-    set_st256((int)value);
-    return TZC_OK;
-  }
-  if (n == "l2_hints") {
-    set_l2_hints((int)value);
-    return TZC_OK;
-  }
-  if (n == "tma_store") {
-    set_tma_store((int)value);
-    return TZC_OK;
-  }
-  return report(Status(TZC_E_VALIDATION, "unknown option '" + n + "'"));
-}
-
-}  // namespace
-
 extern "C" {
 
 int tzc_b200_set_option(const char* name, int64_t value) {
   if (!name) return report(Status(TZC_E_MISSING_INPUT, "NULL option name"));
-  std::lock_guard<std::mutex> lk(g_opt_mu);
-  const int rc = set_option_raw(name, value);
-  if (rc == TZC_OK) g_opt_now[name] = value;
-  return rc;
+  return report(set_default_option(name, value));
 }
 
 int tzc_b200_set_splits(int32_t splits) {
   if (splits < 0) return report(Status(TZC_E_SHAPE, "splits must be >= 0"));
-  set_forced_splits(splits);
-  return TZC_OK;
+  return report(set_default_option("splits", splits));
 }
 
 int tzc_b200_unblock_data(const void* src, void* dst, int32_t c, int32_t h, int32_t w, int32_t cb, int32_t elem_bytes,
@@ -419,14 +289,13 @@ int tune_problem(const std::string& key, Run run, int reps, int apply, char* log
   double best_us = 0, default_us = 0;
   int best = -1;
   for (int c = 0; c < kNumCandidates; ++c) {
-    const Overrides o = parse_overrides(kCandidates[c]);
+    Options o = options_for("");
     float ms = 0;
-    Status s;
+    Status s = parse_option_spec(kCandidates[c], &o, nullptr);
     {
-      ScopedOptions so(o);
-      for (int w = 0; w < 2 && s.ok(); ++w) s = run(st);
+      for (int w = 0; w < 2 && s.ok(); ++w) s = run(o, st);
       if (s.ok()) cudaEventRecord(e0, st);
-      for (int r = 0; r < reps && s.ok(); ++r) s = run(st);
+      for (int r = 0; r < reps && s.ok(); ++r) s = run(o, st);
       if (s.ok()) cudaEventRecord(e1, st);
       if (s.ok() && cudaEventSynchronize(e1) != cudaSuccess) s = Status(TZC_E_DEVICE, "tune: launch failed");
       if (s.ok()) cudaEventElapsedTime(&ms, e0, e1);
@@ -455,11 +324,7 @@ int tune_problem(const std::string& key, Run run, int reps, int apply, char* log
   std::snprintf(line, sizeof line, "best %d %s %.2f us (default %.2f us)\n", best, best ? kCandidates[best] : "default",
                 best_us, default_us);
   text += line;
-  if (apply) {
-    std::lock_guard<std::mutex> lk(g_opt_mu);
-    if (best) g_problem_opts[key] = parse_overrides(kCandidates[best]);
-    else g_problem_opts.erase(key);
-  }
+  if (apply) set_problem_options(key, best ? kCandidates[best] : "");
   if (log && loglen > 0) {
     const size_t n = std::min<size_t>(text.size(), (size_t)loglen - 1);
     std::memcpy(log, text.data(), n);
@@ -485,7 +350,7 @@ int tzc_b200_tune_conv(const tzc_conv_desc* d, const void* x, const void* w, con
   if (!st.ok()) return report(st);
   const tzc_epilogue e = *ep;
   return tune_problem(
-      key_of(*d, 'c'), [&](cudaStream_t s) { return run_problem(pb, x, w, c_seed, out, e, s); }, reps, apply, log,
+      key_of(*d, 'c'), [&](const Options& o, cudaStream_t s) { return run_problem(pb, o, x, w, c_seed, out, e, s); }, reps, apply, log,
       loglen, static_cast<cudaStream_t>(stream));
   TZC_GUARD_END
 }
@@ -503,14 +368,13 @@ int tzc_b200_tune_gemm(const tzc_gemm_desc* d, const void* a, const void* b, con
   if (!st.ok()) return report(st);
   const tzc_epilogue e = *ep;
   return tune_problem(
-      key_of(*d, 'g'), [&](cudaStream_t s) { return run_problem(pb, a, b, c_seed, out, e, s); }, reps, apply, log,
+      key_of(*d, 'g'), [&](const Options& o, cudaStream_t s) { return run_problem(pb, o, a, b, c_seed, out, e, s); }, reps, apply, log,
       loglen, static_cast<cudaStream_t>(stream));
   TZC_GUARD_END
 }
 
 int tzc_b200_clear_tuning(void) {
-  std::lock_guard<std::mutex> lk(g_opt_mu);
-  g_problem_opts.clear();
+  clear_problem_options();
   return TZC_OK;
 }
 
@@ -523,26 +387,14 @@ extern "C" {
 int tzc_b200_set_problem_options_conv(const tzc_conv_desc* d, const char* spec) {
   TZC_GUARD_BEGIN
   if (!d) return report(Status(TZC_E_MISSING_INPUT, "NULL descriptor"));
-  const Overrides o = parse_overrides(spec ? spec : "");
-  for (const auto& kv : o)
-    if (!g_opt_now.count(kv.first)) return report(Status(TZC_E_VALIDATION, "unknown option '" + kv.first + "'"));
-  std::lock_guard<std::mutex> lk(g_opt_mu);
-  if (o.empty()) g_problem_opts.erase(key_of(*d, 'c'));
-  else g_problem_opts[key_of(*d, 'c')] = o;
-  return TZC_OK;
+  return report(set_problem_options(key_of(*d, 'c'), spec ? spec : ""));
   TZC_GUARD_END
 }
 
 int tzc_b200_set_problem_options_gemm(const tzc_gemm_desc* d, const char* spec) {
   TZC_GUARD_BEGIN
   if (!d) return report(Status(TZC_E_MISSING_INPUT, "NULL descriptor"));
-  const Overrides o = parse_overrides(spec ? spec : "");
-  for (const auto& kv : o)
-    if (!g_opt_now.count(kv.first)) return report(Status(TZC_E_VALIDATION, "unknown option '" + kv.first + "'"));
-  std::lock_guard<std::mutex> lk(g_opt_mu);
-  if (o.empty()) g_problem_opts.erase(key_of(*d, 'g'));
-  else g_problem_opts[key_of(*d, 'g')] = o;
-  return TZC_OK;
+  return report(set_problem_options(key_of(*d, 'g'), spec ? spec : ""));
   TZC_GUARD_END
 }
 

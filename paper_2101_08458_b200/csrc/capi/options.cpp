@@ -1,0 +1,155 @@
+// Plan options: the process defaults (tzc_b200_set_option) and the
+// per-descriptor overrides installed by the measured tuner
+// (tzc_b200_tune_* / tzc_b200_set_problem_options_*).
+//
+// A launch never reads shared mutable state while it plans: options_for()
+// copies the defaults and applies the descriptor's overrides under one lock,
+// and the resulting Options value is passed down through plan_problem /
+// run_problem.  Options choose the kernel plan only, never the results.
+#include <cstdlib>
+#include <map>
+#include <mutex>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "../tzc_b200_internal.hpp"
+
+namespace tzcb200 {
+namespace {
+
+// name -> field, legal range; an out-of-range value is rejected (the old
+// behaviour silently clamped, which hid typos in tuning specs).
+struct Knob {
+  const char* name;
+  int Options::*field;
+  int64_t lo, hi;
+  const int* allowed;  // optional explicit set (terminated by -1)
+};
+constexpr int kMtAllowed[] = {0, 1, 2, 4, -1};
+constexpr int kBnAllowed[] = {0, 64, 128, 256, -1};
+constexpr int kEgAllowed[] = {1, 2, -1};
+const Knob kKnobs[] = {
+    {"splits", &Options::splits, 0, 1 << 16, nullptr},
+    {"shifted_window", &Options::shifted_window, 0, 1, nullptr},
+    {"ws_epi_groups", &Options::ws_epi_groups, 1, 2, kEgAllowed},
+    {"tail_split", &Options::tail_split, 0, 1, nullptr},
+    {"split_min_kb", &Options::split_min_kb, 1, 1 << 20, nullptr},
+    {"pingpong_kb", &Options::pingpong_kb, 0, 1 << 20, nullptr},
+    {"ws_mt", &Options::ws_mt, 0, 4, kMtAllowed},
+    {"ws_1x1_k", &Options::ws_1x1_k, 0, 1 << 20, nullptr},
+    {"ws_1x1", &Options::ws_1x1, 0, 1, nullptr},
+    {"bn", &Options::bn, 0, 256, kBnAllowed},
+    {"tma_store_k", &Options::tma_store_k, 0, 1 << 20, nullptr},
+    {"pair_min_kb", &Options::pair_min_kb, 0, 1 << 20, nullptr},
+    {"pair", &Options::pair, 0, 1, nullptr},
+    {"st256", &Options::st256, 0, 1, nullptr},
+    {"l2_hints", &Options::l2_hints, 0, 3, nullptr},
+    {"tma_store", &Options::tma_store, 0, 2, nullptr},
+};
+
+std::mutex g_mu;
+Options g_defaults = [] {
+  Options o;
+  if (std::getenv("TZC_B200_NO_WS")) o.shifted_window = 0;
+  return o;
+}();
+// descriptor key -> validated overrides, applied on the defaults at each call
+std::map<std::string, std::vector<std::pair<std::string, int64_t>>> g_problem;
+
+}  // namespace
+
+bool apply_option(Options* o, const std::string& name, int64_t value, std::string* err) {
+  for (const Knob& k : kKnobs) {
+    if (name != k.name) continue;
+    bool ok = value >= k.lo && value <= k.hi;
+    if (ok && k.allowed) {
+      ok = false;
+      for (const int* a = k.allowed; *a >= 0; ++a) ok = ok || value == *a;
+    }
+    if (!ok) {
+      if (err) *err = "option '" + name + "': illegal value " + std::to_string(value);
+      return false;
+    }
+    o->*k.field = (int)value;
+    return true;
+  }
+  if (err) *err = "unknown option '" + name + "'";
+  return false;
+}
+
+const char* const* option_names() {
+  static const std::vector<const char*> names = [] {
+    std::vector<const char*> v;
+    for (const Knob& k : kKnobs) v.push_back(k.name);
+    v.push_back(nullptr);
+    return v;
+  }();
+  return names.data();
+}
+
+Options options_for(const std::string& key) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  Options o = g_defaults;
+  if (!key.empty()) {
+    auto it = g_problem.find(key);
+    if (it != g_problem.end())
+      for (const auto& [n, v] : it->second) apply_option(&o, n, v, nullptr);
+  }
+  return o;
+}
+
+// "name=value;name=value" applied on top of *out; the items in *items.
+Status parse_option_spec(const std::string& spec, Options* out,
+                         std::vector<std::pair<std::string, int64_t>>* items) {
+  Options o = *out;
+  std::vector<std::pair<std::string, int64_t>> it;
+  size_t i = 0;
+  while (i < spec.size()) {
+    size_t j = spec.find(';', i);
+    if (j == std::string::npos) j = spec.size();
+    const std::string kv = spec.substr(i, j - i);
+    i = j + 1;
+    if (kv.empty()) continue;
+    const size_t eq = kv.find('=');
+    if (eq == std::string::npos) return Status(TZC_E_VALIDATION, "option spec item '" + kv + "' has no '='");
+    int64_t v = 0;
+    try {
+      v = std::stoll(kv.substr(eq + 1));
+    } catch (...) {
+      return Status(TZC_E_VALIDATION, "option spec item '" + kv + "': not an integer");
+    }
+    std::string err;
+    if (!apply_option(&o, kv.substr(0, eq), v, &err)) return Status(TZC_E_VALIDATION, err);
+    it.emplace_back(kv.substr(0, eq), v);
+  }
+  *out = o;
+  if (items) *items = std::move(it);
+  return Status();
+}
+
+Status set_default_option(const std::string& name, int64_t value) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  std::string err;
+  if (!apply_option(&g_defaults, name, value, &err)) return Status(TZC_E_VALIDATION, err);
+  return Status();
+}
+
+// Installs the overrides `spec` for descriptor `key`; an empty spec removes them.
+Status set_problem_options(const std::string& key, const std::string& spec) {
+  Options o;
+  std::vector<std::pair<std::string, int64_t>> items;
+  Status st = parse_option_spec(spec, &o, &items);
+  if (!st.ok()) return st;
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (items.empty()) g_problem.erase(key);
+  else g_problem[key] = std::move(items);
+  return Status();
+}
+
+void clear_problem_options() {
+  std::lock_guard<std::mutex> lk(g_mu);
+  g_problem.clear();
+}
+
+}  // namespace tzcb200

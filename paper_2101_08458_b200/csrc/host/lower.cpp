@@ -600,6 +600,7 @@ void run_tensorized_packed(const TensorizedOp& t, const std::map<std::string, co
   ol.stride_m = p.out_stride_m;
   ol.stride_blk = p.out_stride_blk;
   const tzc_epilogue e{ep.kind, ep.scale};
+  const Options opts = options_for("");  // one plan-option snapshot for every launch of this call
   auto fail = [](const Status& s) {
     if (s.code == TZC_E_DEVICE) throw DeviceError(s.msg);
     throw InjectError(s.msg);
@@ -683,7 +684,7 @@ void run_tensorized_packed(const TensorizedOp& t, const std::map<std::string, co
                 "H2D accumulator image");
       }
       uint8_t* co = static_cast<uint8_t*>(dout) + u0 * per_unit_o * eb_o;
-      const Status s = run_problem(problem(nu), cx, dw, cs, co, e, st);
+      const Status s = run_problem(problem(nu), opts, cx, dw, cs, co, e, st);
       if (!s.ok()) fail(s);
       cuda_ok(cudaMemcpyAsync(static_cast<uint8_t*>(host_out) + u0 * per_unit_o * eb_o, co, nu * per_unit_o * eb_o,
                               cudaMemcpyDeviceToHost, st),
@@ -741,7 +742,7 @@ void run_tensorized_packed(const TensorizedOp& t, const std::map<std::string, co
       const void* b3 = static_cast<const uint8_t*>(uw) + rd * (size_t)(p.r * p.s * p.c) * eb;
       const bool last = rd == p.kd - 1;
       void* o3 = last ? dout : acc[rd & 1];
-      const Status s = run_problem(problem(p.n), a3, b3, seed, o3, last ? e : mid, st);
+      const Status s = run_problem(problem(p.n), opts, a3, b3, seed, o3, last ? e : mid, st);
       if (!s.ok()) fail(s);
       seed = o3;
     }
@@ -749,7 +750,7 @@ void run_tensorized_packed(const TensorizedOp& t, const std::map<std::string, co
     cuda_ok(cudaStreamSynchronize(st), "tensorized op");
     return;
   }
-  const Status s = run_problem(problem(p.family == KernelPlan::Family::Matmul ? p.m : p.n), a, b, ds, dout, e, st);
+  const Status s = run_problem(problem(p.family == KernelPlan::Family::Matmul ? p.m : p.n), opts, a, b, ds, dout, e, st);
   if (!s.ok()) fail(s);
   cuda_ok(cudaMemcpyAsync(host_out, dout, (size_t)out_bytes, cudaMemcpyDeviceToHost, st), "D2H output");
   cuda_ok(cudaStreamSynchronize(st), "tensorized op");

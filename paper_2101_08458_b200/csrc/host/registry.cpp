@@ -1,11 +1,21 @@
 // tzc host library, part 2: the instruction-semantics registry.
-// Same contract as the reference (/root/reference/proj/src/intrinsics.cpp:
-// Intrinsic::accumulator :35-57, validate_intrinsic :59-101, .intr grammar
-// :185-272, resolve :287-296), with the sm_100a tcgen05 descriptions added as
-// builtins.  The tcgen05 texts are ordinary .intr programs in the reference's
-// own grammar (they pass the reference's parse/inspect/inject
-// unmodified).
+//
+// An instruction description (SPEC.md "Intrinsic definition file (.intr)") is
+// three kinds of line: the semantics block in the .tdsl grammar (parsed by
+// parse_compute), one "rule <register>: kind(loop) ..." line per input
+// register saying how its lanes are filled from memory, and one
+// `mnemonic "<text>"` line naming the target instruction.  Entry points
+// replaced: /root/reference/proj/include/tzc/intrinsics.hpp:15-65 (same
+// names, arguments and error kinds: SyntaxError for malformed lines,
+// RuleError for rules inconsistent with the semantics, UnknownIntrinsic /
+// IoError from resolve / load).
+//
+// Builtins: the reference's three CPU descriptions (restated below in the
+// .intr grammar) plus the sm_100a tcgen05.mma descriptions this backend
+// executes.  The tcgen05 texts are ordinary .intr programs (SURVEY.md F5:
+// the reference's own parse / inspect / inject accept them unmodified).
 #include <cctype>
+#include <cstring>
 #include <fstream>
 #include <map>
 #include <set>
@@ -32,11 +42,12 @@ const std::vector<OperandRule>* Intrinsic::rules_for(const std::string& t) const
 }
 
 namespace {
+// Does expression e load tensor t at exactly the index list idx anywhere?
 bool loads_at(const ExprPtr& e, const std::string& t, const std::vector<ExprPtr>& idx) {
   if (e->kind == Expr::Kind::Load && e->name == t && e->args.size() == idx.size()) {
-    bool same = true;
-    for (size_t i = 0; i < idx.size(); ++i) same = same && expr_equal(e->args[i], idx[i], false);
-    if (same) return true;
+    size_t i = 0;
+    while (i < idx.size() && expr_equal(e->args[i], idx[i], false)) ++i;
+    if (i == idx.size()) return true;
   }
   for (const auto& a : e->args)
     if (loads_at(a, t, idx)) return true;
@@ -44,6 +55,8 @@ bool loads_at(const ExprPtr& e, const std::string& t, const std::vector<ExprPtr>
 }
 }  // namespace
 
+// The register the instruction accumulates into: the output for "+=" forms,
+// else the input read at the store's own index (d[i] = c[i] + ...).
 std::string Intrinsic::accumulator() const {
   if (semantics.update) return semantics.out;
   for (const auto& t : semantics.tensors)
@@ -51,102 +64,122 @@ std::string Intrinsic::accumulator() const {
   return "";
 }
 
+// Consistency of the operand rules with the semantics: every input register
+// has exactly one non-empty rule list; each rule names a loop of the
+// semantics and spans its whole extent; the lanes the rules enumerate are
+// exactly the register's element count.
 void validate_intrinsic(const Intrinsic& intr) {
-  if (intr.name.empty()) throw RuleError("intrinsic without a name");
+  if (intr.name.empty()) throw RuleError("an intrinsic needs a name");
   validate(intr.semantics);
   if (intr.requires_inplace_acc != intr.semantics.update)
-    throw RuleError("requires_inplace_acc must mirror accumulate-form semantics");
-  std::set<std::string> seen;
-  for (const auto& [tensor, rules] : intr.operand_rules) {
-    const TensorDecl* t = intr.semantics.find_tensor(tensor);
-    if (!t) throw RuleError("rule for unknown tensor '" + tensor + "'");
-    if (t->role != Role::Input) throw RuleError("rule for non-input tensor '" + tensor + "'");
-    if (!seen.insert(tensor).second) throw RuleError("duplicate rule for tensor '" + tensor + "'");
-    if (rules.empty()) throw RuleError("empty rule list for tensor '" + tensor + "'");
+    throw RuleError("requires_inplace_acc must equal the semantics' update (+=) form");
+  std::map<std::string, const TensorDecl*> pending;  // input registers still without rules
+  for (const auto& t : intr.semantics.tensors)
+    if (t.role == Role::Input) pending[t.name] = &t;
+  std::set<std::string> ruled;
+  for (const auto& [reg, rules] : intr.operand_rules) {
+    const TensorDecl* t = intr.semantics.find_tensor(reg);
+    const std::string where = "operand rules of '" + reg + "'";
+    if (!t) throw RuleError(where + ": no such tensor in the semantics");
+    if (t->role != Role::Input) throw RuleError(where + ": only input registers take rules");
+    if (!ruled.insert(reg).second) throw RuleError(where + ": given twice");
+    if (rules.empty()) throw RuleError(where + ": empty");
+    pending.erase(reg);
     int64_t lanes = 1;
     for (const auto& r : rules) {
       if (r.kind == OperandRule::Kind::Passthrough) {
-        if (!r.loop.empty()) throw RuleError("passthrough takes no loop argument");
+        if (!r.loop.empty()) throw RuleError(where + ": passthrough has no loop argument");
         continue;
       }
       const LoopVar* l = intr.semantics.find_loop(r.loop);
-      if (!l) throw RuleError("rule on tensor '" + tensor + "' references unknown loop '" + r.loop + "'");
+      if (!l) throw RuleError(where + ": loop '" + r.loop + "' is not a loop of the semantics");
       if (r.count != l->extent)
-        throw RuleError("rule count " + std::to_string(r.count) + " on '" + tensor + "' must equal extent of loop '" +
-                        r.loop + "' (" + std::to_string(l->extent) + ")");
+        throw RuleError(where + ": " + OperandRule::kind_name(r.kind) + "(" + r.loop + ") spans " +
+                        std::to_string(r.count) + " lanes, the loop's extent is " + std::to_string(l->extent));
       lanes *= r.count;
     }
     if (lanes != t->size())
-      throw RuleError("rules on '" + tensor + "' cover " + std::to_string(lanes) + " lanes but the register holds " +
-                      std::to_string(t->size()));
+      throw RuleError(where + ": the rules enumerate " + std::to_string(lanes) + " lanes, the register has " +
+                      std::to_string(t->size()) + " elements");
   }
-  for (const auto& t : intr.semantics.tensors)
-    if (t.role == Role::Input && !seen.count(t.name)) throw RuleError("input tensor '" + t.name + "' has no operand rule");
+  if (!pending.empty()) throw RuleError("input register '" + pending.begin()->first + "' has no operand rules");
 }
 
-Intrinsic parse_intrinsic(const std::string& text, const std::string& name) {
-  std::string sem;
-  std::vector<std::string> rule_lines;
-  std::string mnemonic;
-  bool have_mnemonic = false;
-  std::istringstream in(text);
-  std::string line;
-  while (std::getline(in, line)) {
-    const size_t b = line.find_first_not_of(" \t");
-    const std::string t = b == std::string::npos ? "" : line.substr(b);
-    if (t.rfind("rule", 0) == 0) {
-      rule_lines.push_back(t);
-    } else if (t.rfind("mnemonic", 0) == 0) {
-      const size_t q1 = t.find('"'), q2 = t.rfind('"');
-      if (q1 == std::string::npos || q2 <= q1) throw SyntaxError("mnemonic line must carry a quoted string");
-      mnemonic = t.substr(q1 + 1, q2 - q1 - 1);
-      have_mnemonic = true;
-    } else {
-      sem += line + "\n";
+namespace {
+
+std::string strip(const std::string& s) {
+  const size_t b = s.find_first_not_of(" \t\r");
+  if (b == std::string::npos) return "";
+  return s.substr(b, s.find_last_not_of(" \t\r") - b + 1);
+}
+
+bool starts_with(const std::string& s, const char* word) { return s.compare(0, std::strlen(word), word) == 0; }
+
+// "rule <register>: kind(loop) kind(loop) ..." -> (register, rules); the
+// lane counts are filled from the semantics' loop extents (0 for a loop the
+// semantics lacks, which validate_intrinsic then reports).
+std::pair<std::string, std::vector<OperandRule>> parse_rule_line(const std::string& line, const ComputeOp& sem) {
+  const std::string body = line.substr(4);  // after "rule"
+  const size_t colon = body.find(':');
+  if (colon == std::string::npos) throw SyntaxError("rule line '" + line + "': expected 'rule <register>: ...'");
+  const std::string reg = strip(body.substr(0, colon));
+  if (reg.empty()) throw SyntaxError("rule line '" + line + "': missing register name");
+  static const std::map<std::string, OperandRule::Kind> kinds = {
+      {"vectorize", OperandRule::Kind::Vectorize},
+      {"broadcast", OperandRule::Kind::Broadcast},
+      {"unroll_concat", OperandRule::Kind::UnrollConcat},
+      {"passthrough", OperandRule::Kind::Passthrough}};
+  std::vector<OperandRule> rules;
+  std::istringstream words(body.substr(colon + 1));
+  for (std::string w; words >> w;) {
+    const size_t open = w.find('(');
+    const std::string kw = w.substr(0, open);
+    auto k = kinds.find(kw);
+    if (k == kinds.end()) throw SyntaxError("rule line '" + line + "': unknown rule kind '" + kw + "'");
+    OperandRule r;
+    r.kind = k->second;
+    if (r.kind != OperandRule::Kind::Passthrough) {
+      if (open == std::string::npos || w.back() != ')')
+        throw SyntaxError("rule line '" + line + "': " + kw + " takes a loop, as " + kw + "(<loop>)");
+      r.loop = w.substr(open + 1, w.size() - open - 2);
+      const LoopVar* l = sem.find_loop(r.loop);
+      r.count = l ? l->extent : 0;
     }
+    rules.push_back(std::move(r));
   }
-  if (!have_mnemonic) throw SyntaxError("intrinsic description lacks a mnemonic");
+  return {reg, std::move(rules)};
+}
+
+}  // namespace
+
+Intrinsic parse_intrinsic(const std::string& text, const std::string& name) {
+  std::string semantics;
+  std::vector<std::string> rule_lines;
+  std::vector<std::string> mnemonics;
+  std::istringstream in(text);
+  for (std::string raw; std::getline(in, raw);) {
+    const std::string t = strip(raw);
+    if (starts_with(t, "rule"))
+      rule_lines.push_back(t);
+    else if (starts_with(t, "mnemonic"))
+      mnemonics.push_back(t);
+    else
+      semantics += raw + "\n";  // everything else is the .tdsl block
+  }
+  if (mnemonics.empty()) throw SyntaxError("instruction description '" + name + "' has no mnemonic line");
+  std::string mnemonic;
+  for (const auto& m : mnemonics) {  // the last one wins
+    const size_t first = m.find('"'), last = m.rfind('"');
+    if (first == std::string::npos || last == first)
+      throw SyntaxError("mnemonic line '" + m + "': expected mnemonic \"<text>\"");
+    mnemonic = m.substr(first + 1, last - first - 1);
+  }
   Intrinsic intr;
   intr.name = name;
-  intr.semantics = infer_types(parse_compute(sem));
+  intr.semantics = infer_types(parse_compute(semantics));
   intr.target_mnemonic = mnemonic;
   intr.requires_inplace_acc = intr.semantics.update;
-  for (const auto& rl : rule_lines) {
-    // rule <tensor>: kind(loop) kind(loop) ...
-    std::string body = rl.substr(4);
-    const size_t colon = body.find(':');
-    if (colon == std::string::npos) throw SyntaxError("rule line without ':'");
-    std::string tensor = body.substr(0, colon);
-    tensor.erase(0, tensor.find_first_not_of(" \t"));
-    tensor.erase(tensor.find_last_not_of(" \t") + 1);
-    if (tensor.empty()) throw SyntaxError("rule line without tensor name");
-    std::istringstream items(body.substr(colon + 1));
-    std::vector<OperandRule> rules;
-    std::string item;
-    while (items >> item) {
-      OperandRule r;
-      const size_t p = item.find('(');
-      const std::string kind = p == std::string::npos ? item : item.substr(0, p);
-      if (kind == "vectorize")
-        r.kind = OperandRule::Kind::Vectorize;
-      else if (kind == "broadcast")
-        r.kind = OperandRule::Kind::Broadcast;
-      else if (kind == "unroll_concat")
-        r.kind = OperandRule::Kind::UnrollConcat;
-      else if (kind == "passthrough")
-        r.kind = OperandRule::Kind::Passthrough;
-      else
-        throw SyntaxError("unknown rule kind '" + kind + "'");
-      if (r.kind != OperandRule::Kind::Passthrough) {
-        if (p == std::string::npos || item.back() != ')') throw SyntaxError("rule '" + kind + "' needs a loop argument");
-        r.loop = item.substr(p + 1, item.size() - p - 2);
-        const LoopVar* l = intr.semantics.find_loop(r.loop);
-        r.count = l ? l->extent : 0;
-      }
-      rules.push_back(std::move(r));
-    }
-    intr.operand_rules.emplace_back(tensor, std::move(rules));
-  }
+  for (const auto& rl : rule_lines) intr.operand_rules.push_back(parse_rule_line(rl, intr.semantics));
   validate_intrinsic(intr);
   return intr;
 }

@@ -37,14 +37,9 @@ constexpr int kStaticSmem = 0;
 #endif
 // General-kernel SMEM: EG int8 staging tiles (128 x BN) + the A/B ring + barriers.
 int ring_smem(int bn, int kb, int eg, int stages) { return 1024 + eg * 128 * bn + stages * (128 + bn) * kb + 256; }
-// set_option "split_min_kb": automatic split-K for under-filled grids keeps
-// >= this many K blocks per split.  Off by default: in the multi-branch
-// graph step other layers' CTAs fill idle SMs, and the int32 partial round
-// trip + fix-up launch cost more (batch 32: 511 -> 572 TOPS without it,
-// batch 64: 660 -> 804).
-int g_split_min_kb = 1 << 20;
-int g_pingpong_kb = 2;  // set_option "pingpong_kb": max K blocks per tile for ping-pong epilogue groups
-int epi_groups_for(int kb_per_tile) { return kb_per_tile <= g_pingpong_kb ? 2 : 1; }
+using tzcb200::Options;
+// Ping-pong epilogue groups for tiles of <= o.pingpong_kb K blocks.
+int epi_groups_for(int kb_per_tile, const Options& o) { return kb_per_tile <= o.pingpong_kb ? 2 : 1; }
 
 // How the tiles are cut along K.  none: every unit a whole tile.  classic
 // split-K (fewer tiles than SMs): every tile split.  tail split: the last,
@@ -56,8 +51,12 @@ struct WorkSplit {
   int splits = 1;
   int full = 0;  // whole-tile units (they come first)
 };
-int g_tail_split = 0;  // set_option "tail_split" (measured slower with the separate fix-up kernel)
-WorkSplit work_split(int tiles, int tiles_n, int num_kb, int sms, bool ok16, int forced) {
+// "split_min_kb": automatic split-K for under-filled grids keeps >= this many
+// K blocks per split.  Off by default: in the multi-branch graph step other
+// layers' CTAs fill idle SMs, and the int32 partial round trip + fix-up
+// launch cost more (batch 32: 511 -> 572 TOPS without it, batch 64: 660 ->
+// 804).  "tail_split": measured slower with the separate fix-up kernel.
+WorkSplit work_split(int tiles, int tiles_n, int num_kb, int sms, bool ok16, int forced, const Options& o) {
   WorkSplit w;
   w.full = tiles;
   if (forced > 0) {
@@ -69,7 +68,7 @@ WorkSplit work_split(int tiles, int tiles_n, int num_kb, int sms, bool ok16, int
   if (tiles < sms) {
     // fill the machine, keeping >= 8 K blocks per split so the int32 partial
     // round trip stays small next to the MMA work
-    const int s = std::min((sms + tiles - 1) / tiles, num_kb / g_split_min_kb);
+    const int s = std::min((sms + tiles - 1) / tiles, num_kb / std::max(1, o.split_min_kb));
     if (s >= 2) {
       w.splits = s;
       w.full = 0;
@@ -77,7 +76,7 @@ WorkSplit work_split(int tiles, int tiles_n, int num_kb, int sms, bool ok16, int
     return w;
   }
   const int tail = tiles % sms;
-  if (g_tail_split && tail > 0 && 2 * tail <= sms && num_kb >= 8) {
+  if (o.tail_split && tail > 0 && 2 * tail <= sms && num_kb >= 8) {
     int full = tiles - tail;
     full -= full % tiles_n;  // the split region starts on an M-tile boundary
     const int s = std::min(num_kb / 4, sms / (tiles - full));
@@ -116,8 +115,6 @@ PFN_cuTensorMapEncodeTiled_v12000 p_encode_tiled = nullptr;
 PFN_cuTensorMapEncodeIm2col_v12000 p_encode_im2col = nullptr;
 std::once_flag g_driver_once;
 int g_driver_version = 0;
-int g_num_sms = 0;
-int g_dev_ok = -1;
 
 Status load_driver() {
   std::call_once(g_driver_once, [] {
@@ -141,23 +138,53 @@ Status load_driver() {
 
 }  // namespace
 
-int device_ok() {
-  if (g_dev_ok >= 0) return g_dev_ok;
+// Per-device facts, cached by device ordinal (a process may drive several
+// B200s, one host thread and stream each: SURVEY.md §3.5 step 6).
+namespace {
+constexpr int kMaxDev = 64;
+std::atomic<int> g_dev_state[kMaxDev];  // 0 unknown; low byte 1 = sm_100, 2 = unusable; SM count << 8
+int current_device() {
   int dev = 0;
-  cudaDeviceProp prop;
-  if (cudaGetDevice(&dev) != cudaSuccess || cudaGetDeviceProperties(&prop, dev) != cudaSuccess) {
+  if (cudaGetDevice(&dev) != cudaSuccess) {
     cudaGetLastError();
-    g_dev_ok = 0;
-    return 0;
+    return -1;
   }
-  g_num_sms = prop.multiProcessorCount;
-  g_dev_ok = (prop.major == 10 && prop.minor == 0) ? 1 : 0;
-  return g_dev_ok;
+  return dev < kMaxDev ? dev : -1;
+}
+int dev_state(int dev) {
+  if (dev < 0) return 2;
+  int st = g_dev_state[dev].load(std::memory_order_acquire);
+  if (st) return st;
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, dev) != cudaSuccess) {
+    cudaGetLastError();
+    st = 2;
+  } else {
+    st = ((prop.major == 10 && prop.minor == 0) ? 1 : 2) | (prop.multiProcessorCount << 8);
+  }
+  g_dev_state[dev].store(st, std::memory_order_release);
+  return st;
 }
 
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) is per device: one bit per
+// device ordinal per kernel instantiation.
+template <typename Kern>
+Status ensure_smem_attr(Kern kern, std::atomic<uint64_t>& done) {
+  const int dev = current_device();
+  const uint64_t bit = dev >= 0 ? (uint64_t(1) << dev) : 0;
+  if (bit && (done.load(std::memory_order_acquire) & bit)) return Status();
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024 - kStaticSmem);
+  if (e != cudaSuccess) return Status(TZC_E_DEVICE, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
+  done.fetch_or(bit, std::memory_order_acq_rel);
+  return Status();
+}
+}  // namespace
+
+int device_ok() { return (dev_state(current_device()) & 0xff) == 1 ? 1 : 0; }
+
 int num_sms() {
-  device_ok();
-  return g_num_sms > 0 ? g_num_sms : 148;
+  const int st = dev_state(current_device());
+  return (st >> 8) > 0 ? (st >> 8) : 148;
 }
 
 namespace {
@@ -185,12 +212,9 @@ cudaError_t launch_pdl(Kern kern, dim3 grid, dim3 block, size_t smem, cudaStream
 template <int BN, int KB, bool F16, int AM, bool BMN, int EPM>
 Status launch_kernel(const ConvKernelParams& p, int grid, cudaStream_t stream) {
   auto kern = tzcdev::conv_tc_kernel<BN, KB, F16, AM, BMN, EPM>;
-  static bool attr_done = false;  // per instantiation
-  if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024 - kStaticSmem);
-    if (e != cudaSuccess) return Status(TZC_E_DEVICE, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
-    attr_done = true;
-  }
+  static std::atomic<uint64_t> attr_done{0};  // per instantiation, one bit per device
+  Status sa = ensure_smem_attr(kern, attr_done);
+  if (!sa.ok()) return sa;
   const int smem = ring_smem(BN, KB, p.tma_store ? p.epi_groups : 0, p.stages);  // staging only for TMA stores
   cudaError_t e = launch_pdl(kern, dim3(grid), dim3(tzcdev::EpiCfg<BN>::THREADS), smem, stream, p);
   g_launches.fetch_add(1, std::memory_order_relaxed);
@@ -206,12 +230,9 @@ int pair_stages(int bn) { return std::min(8, (227 * 1024 - kStaticSmem - 1024 - 
 template <int BN, int AM>
 Status launch_pair(const ConvKernelParams& p, int grid, cudaStream_t stream) {
   auto kern = tzcdev::conv_tc2_kernel<BN, AM>;
-  static bool attr_done = false;
-  if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024 - kStaticSmem);
-    if (e != cudaSuccess) return Status(TZC_E_DEVICE, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
-    attr_done = true;
-  }
+  static std::atomic<uint64_t> attr_done{0};  // per instantiation, one bit per device
+  Status sa = ensure_smem_attr(kern, attr_done);
+  if (!sa.ok()) return sa;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(tzcdev::EpiCfg<BN>::THREADS);
@@ -314,77 +335,44 @@ Status enc_check(CUresult r, const char* what) {
   return Status();
 }
 
-// Device scratch, cached per (stream, slot) — slot 0: split-K partials,
-// 1: K7 im2col rows, 2: K7 padded weights.  Per stream so that independent
-// ops captured on parallel graph branches never share scratch; launches on
-// one stream are ordered, so reuse within a stream is safe.  Grown outside
-// timed loops (first use).
+// Device scratch, cached per (device, stream, slot) — slot 0: split-K
+// partials, 1: K7 im2col rows / S2D pixels, 2: K7 padded / S2D weights.  Per
+// stream so that independent ops captured on parallel graph branches never
+// share scratch; launches on one stream are ordered, so reuse within a stream
+// is safe.  A buffer that has to grow is RETIRED, not freed: a CUDA graph
+// captured earlier on this stream may still hold its address, and freeing it
+// would make that graph's next replay read freed memory.  Growth is
+// geometric, so the retired bytes stay below the live ones.
 std::mutex g_ws_mu;
 struct Scratch {
   void* p[3] = {nullptr, nullptr, nullptr};
   size_t bytes[3] = {0, 0, 0};
 };
-std::map<cudaStream_t, Scratch> g_ws;
-int g_ws_epi_groups = 1;  // shifted-window epilogue groups (set_option "ws_epi_groups")
-// TMA-store int8 epilogue (set_option "tma_store": 0 never, 1 always, 2 = GEMM
-// K of at most g_tma_store_k bytes).  Since the direct epilogue writes whole
-// 32-byte sectors with 256-bit row stores it wins in the multi-branch suite
-// (b256: always 1273, K <= 64 only 1324, never 1333 TOPS), although the
-// K = 64 layer alone is faster with TMA stores (c2_1x1_64_256 96 -> 89 us).
-int g_tma_store = 0;
-int g_tma_store_k = 64;
-// set_option "pair": CTA-pair (cta_group::2) kernel for eligible int8 layers
-// with >= g_pair_min_kb K blocks ("pair_min_kb").  It wins on the deep-K
-// layers (3x3 at 14x14 / 7x7: 2-3 us each) and loses on K <= 1 KiB ones,
-// where the pair's coupled pipelines (one MMA issuer, both epilogues on the
-// leader's barrier) cost more than the halved B stream saves.  Off by
-// default: in the multi-branch suite the per-layer gains do not carry over
-// (b256 1325 -> 1315 TOPS, b32 654 -> 637): a cluster needs two free SMs of
-// one TPC, so pair CTAs fill the SMs other branches leave idle less well.
-int g_pair = 0;
-int g_pair_min_kb = 16;
-int g_st256 = 1;      // set_option "st256": 256-bit epilogue stores where aligned
-int g_l2_hints = 1;    // set_option "l2_hints": 1 = A loads evict-first (default), 2 = B loads evict-last
-int g_forced_bn = 0;   // set_option "bn" (0 = automatic)
-int g_ws_mt = 0;       // set_option "ws_mt": force the shifted-window tiles per unit (0 = automatic)
-int g_ws_1x1 = 0;      // set_option "ws_1x1": force the weight-stationary kernel for every 1x1 stride-1 conv
-int g_ws_1x1_k = 64;   // set_option "ws_1x1_k": ... and for 1x1 convs with K <= this many bytes
-int g_forced_splits = 0;
-int g_ws_enabled = 1;  // shifted-window kernel for eligible stride-1 convs (TZC_B200_NO_WS=1 disables)
+std::map<std::pair<int, cudaStream_t>, Scratch> g_ws;
+std::vector<void*> g_ws_retired;
 
 Status workspace(int slot, size_t bytes, void** out, cudaStream_t stream) {
   std::lock_guard<std::mutex> lk(g_ws_mu);
-  Scratch& s = g_ws[stream];
+  Scratch& s = g_ws[{current_device(), stream}];
   if (bytes > s.bytes[slot]) {
-    if (s.p[slot]) cudaFree(s.p[slot]);
-    s.p[slot] = nullptr;
-    s.bytes[slot] = 0;
-    cudaError_t e = cudaMalloc(&s.p[slot], bytes);
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(stream, &cap) == cudaSuccess && cap != cudaStreamCaptureStatusNone)
+      return Status(TZC_E_DEVICE,
+                    "workspace: scratch must grow while the stream is being captured; run the op once eagerly "
+                    "on this stream before capturing it");
+    const size_t want = std::max(bytes, s.bytes[slot] + s.bytes[slot] / 2);
+    void* p = nullptr;
+    cudaError_t e = cudaMalloc(&p, want);
     if (e != cudaSuccess) return Status(TZC_E_DEVICE, std::string("workspace: ") + cudaGetErrorString(e));
-    s.bytes[slot] = bytes;
+    if (s.p[slot]) g_ws_retired.push_back(s.p[slot]);
+    s.p[slot] = p;
+    s.bytes[slot] = want;
   }
   *out = s.p[slot];
   return Status();
 }
 
 }  // namespace
-
-void set_forced_splits(int s) { g_forced_splits = s; }
-void set_tail_split(int on) { g_tail_split = on ? 1 : 0; }
-void set_ws_enabled(int on) { g_ws_enabled = on; }
-void set_tma_store(int on) { g_tma_store = on < 0 ? 0 : (on > 2 ? 2 : on); }
-void set_tma_store_k(int k) { g_tma_store_k = k; }
-void set_l2_hints(int h) { g_l2_hints = h & 3; }
-void set_st256(int on) { g_st256 = on ? 1 : 0; }
-void set_pair(int on) { g_pair = on ? 1 : 0; }
-void set_pair_min_kb(int kb) { g_pair_min_kb = kb; }
-void set_ws_1x1(int on) { g_ws_1x1 = on ? 1 : 0; }
-void set_ws_1x1_k(int k) { g_ws_1x1_k = k; }
-void set_pingpong_kb(int kb) { g_pingpong_kb = kb; }
-void set_split_min_kb(int kb) { g_split_min_kb = kb < 1 ? 1 : kb; }
-void set_ws_mt(int mt) { g_ws_mt = (mt == 1 || mt == 2 || mt == 4) ? mt : 0; }
-void set_forced_bn(int bn) { g_forced_bn = (bn == 64 || bn == 128 || bn == 256) ? bn : 0; }
-void set_ws_epi_groups(int g) { g_ws_epi_groups = g == 1 ? 1 : 2; }
 
 // ---- K7 (thin-channel) rewrite ------------------------------------------------
 bool needs_k7(const Problem& pb) { return pb.b_kn == 0 && ((int64_t)pb.c * (pb.f16 ? 2 : 1)) % 16 != 0; }
@@ -418,18 +406,33 @@ struct WsPlan {
   int halo = 0;
   int64_t p_rows = 0;
 };
-bool ws_plan(const Problem& pb, bool pair, WsPlan* w);
+bool ws_plan(const Problem& pb, bool pair, const Options& o, WsPlan* w);
 bool s2d_eligible(const Problem& pb);
 Problem s2d_problem(const Problem& pb);
 
+// The one routing decision shared by planning and launch: does this problem
+// run on the weight-stationary shifted-window kernel (q = the problem it
+// runs, the space-to-depth rewrite for the stem)?  A forced split-K (the
+// op's split_reduction schedule or the "splits" option) runs on the general
+// kernel, which implements it; so does everything the ws kernel cannot hold.
+bool ws_route(const Problem& pb, const Options& o, Problem* q, WsPlan* w, bool* s2d) {
+  const bool k7 = needs_k7(pb);
+  const int forced = pb.forced_splits ? pb.forced_splits : o.splits;
+  *s2d = k7 && s2d_eligible(pb);
+  if (forced >= 2) return false;
+  if (!*s2d && (k7 || !o.shifted_window)) return false;
+  *q = *s2d ? s2d_problem(pb) : pb;
+  return ws_plan(*q, *s2d && !pb.f16, o, w);
+}
+
 // ---- planning ----------------------------------------------------------------
-Status plan_problem(const Problem& pb_in, tzc_plan* plan) {
+Status plan_problem(const Problem& pb_in, const Options& o, tzc_plan* plan) {
   {
     // the shifted-window kernel (a_mode 2) and the space-to-depth stem (a_mode 3)
-    const bool s2d = needs_k7(pb_in) && s2d_eligible(pb_in);
-    const Problem q = s2d ? s2d_problem(pb_in) : pb_in;
+    bool s2d = false;
+    Problem q;
     WsPlan w;
-    if ((s2d || (!needs_k7(pb_in) && g_ws_enabled && pb_in.forced_splits < 2)) && ws_plan(q, s2d && !pb_in.f16, &w)) {
+    if (ws_route(pb_in, o, &q, &w, &s2d)) {
       plan->bm = 128 * w.mt;  // rows per work unit
       plan->bn = w.bn;
       plan->bk_bytes = w.kb;
@@ -464,14 +467,14 @@ Status plan_problem(const Problem& pb_in, tzc_plan* plan) {
   // binding resource for these layers (ncu: L2-throughput-bound at BN=64).
   int bn = pb.ngemm % 256 == 0 ? 256 : (pb.ngemm % 128 == 0 ? 128 : 64);
   if (pb.b_kn) bn = pb.ngemm % 128 == 0 ? 128 : 64;  // MN-major path instantiated for 64/128
-  if (g_forced_bn && pb.ngemm % g_forced_bn == 0 && !(pb.b_kn && g_forced_bn == 256)) bn = g_forced_bn;
+  if (o.bn && pb.ngemm % o.bn == 0 && !(pb.b_kn && o.bn == 256)) bn = o.bn;
   const int sms = num_sms();
   const int tiles_m = (int)((M + 127) / 128);
   const int tiles_n = (pb.ngemm + bn - 1) / bn;
   const int num_kb = (int)(pb.taps * ((krow_bytes + kb - 1) / kb));
   const int tiles = tiles_m * tiles_n;
   const WorkSplit wsplit =
-      work_split(tiles, tiles_n, num_kb, sms, pb.ngemm % 16 == 0, pb.forced_splits ? pb.forced_splits : g_forced_splits);
+      work_split(tiles, tiles_n, num_kb, sms, pb.ngemm % 16 == 0, pb.forced_splits ? pb.forced_splits : o.splits, o);
   const int splits = wsplit.splits;
   const int64_t red_m0 = (int64_t)(wsplit.full / tiles_n) * 128;
   const Entry* ent = find_entry(bn, kb, pb.f16, pb.a_mode, pb.b_kn);
@@ -481,7 +484,7 @@ Status plan_problem(const Problem& pb_in, tzc_plan* plan) {
   plan->bk_bytes = kb;
   // ping-pong epilogue groups where the epilogue dominates (one K block
   // per tile); otherwise one group and the deepest ring
-  const int eg = epi_groups_for(num_kb / splits);
+  const int eg = epi_groups_for(num_kb / splits, o);
   plan->stages = ring_stages(bn, kb, eg);
   plan->a_mode = pb.a_mode;
   plan->splits = splits;
@@ -494,7 +497,8 @@ Status plan_problem(const Problem& pb_in, tzc_plan* plan) {
 }
 
 // Output layout, seed and fused-epilogue fields shared by both kernels.
-void fill_epilogue(ConvKernelParams* pp, const Problem& pb, const void* seed, void* out, const tzc_epilogue& ep);
+void fill_epilogue(ConvKernelParams* pp, const Problem& pb, const Options& o, const void* seed, void* out,
+                   const tzc_epilogue& ep);
 // ---- weight-stationary shifted-window path (conv_ws.cuh) --------------------------
 
 namespace {
@@ -529,12 +533,9 @@ int ws_smem(const WsPlan& w, int taps) {
 template <int BN, int KB, bool F16, bool PAIR, int EPM>
 Status launch_ws_kernel(const ConvKernelParams& p, int grid, int smem, cudaStream_t stream) {
   auto kern = tzcdev::conv_ws_kernel<BN, KB, F16, PAIR, EPM>;
-  static int attr_smem = 0;
-  if (attr_smem < smem) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024 - kStaticSmem);
-    if (e != cudaSuccess) return Status(TZC_E_DEVICE, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
-    attr_smem = 227 * 1024 - kStaticSmem;
-  }
+  static std::atomic<uint64_t> attr_done{0};  // per instantiation, one bit per device
+  Status sa = ensure_smem_attr(kern, attr_done);
+  if (!sa.ok()) return sa;
   cudaError_t e = launch_pdl(kern, dim3(grid), dim3(tzcdev::EpiCfg<BN>::THREADS), smem, stream, p);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   if (e == cudaSuccess) e = cudaGetLastError();
@@ -574,15 +575,15 @@ WsFn ws_fn(int bn, int kb, bool f16, bool pair) {
 
 // Eligibility + resources of the shifted-window kernel for a stride-1 conv
 // (pair = 16-byte pixels, the space-to-depth stem).
-bool ws_plan(const Problem& pb, bool pair, WsPlan* w) {
+bool ws_plan(const Problem& pb, bool pair, const Options& o, WsPlan* w) {
   if (pb.b_kn || pb.stride != 1 || needs_k7(pb)) return false;
   // 1x1: weight-stationary pays off only for a single 64-wide N tile and one
   // K block (c2_1x1_64_64: 43 -> 31 us at batch 256); wider layers keep the
   // TMA-store general kernel (measured, tools/layer_timing.py --opt ws_1x1=1)
   // With the direct 256-bit-store epilogue the single-K-block 1x1 layers of
   // any width gain too (c2_1x1_64_256: 96 -> 76 us): "ws_1x1_k" bytes of K.
-  if (pb.taps < 2 && !g_ws_1x1 && !(pb.ngemm == 64 && (int64_t)pb.c * (pb.f16 ? 2 : 1) <= 128) &&
-      !((int64_t)pb.c * (pb.f16 ? 2 : 1) <= g_ws_1x1_k))
+  if (pb.taps < 2 && !o.ws_1x1 && !(pb.ngemm == 64 && (int64_t)pb.c * (pb.f16 ? 2 : 1) <= 128) &&
+      !((int64_t)pb.c * (pb.f16 ? 2 : 1) <= o.ws_1x1_k))
     return false;
   if (!(pb.ngemm == 64 || pb.ngemm == 128 || pb.ngemm == 256)) return false;
   const int e = pb.f16 ? 2 : 1;
@@ -611,12 +612,14 @@ bool ws_plan(const Problem& pb, bool pair, WsPlan* w) {
   const int sms = num_sms();
   // MT tiles per unit: the largest that fits TMEM (2*MT*BN <= 512) and SMEM
   // (>= 2 super-tile slots next to the resident weights), keeps every CTA
-  // busy for >= 8 units and loses <= 6% to the last round's imbalance
+  // busy for >= 8 units and loses <= 6% to the last round's imbalance.  A
+  // forced "ws_mt" skips the occupancy rules (only the resources bind), so
+  // tests can run every MT at small batches.
   for (int mt : {4, 2, 1}) {
     if (2 * mt * x.bn > 512) continue;
-    if (g_ws_mt && mt != g_ws_mt) continue;
+    if (o.ws_mt && mt != o.ws_mt) continue;
     const int units = (tiles + mt - 1) / mt;
-    if (mt > 1) {
+    if (mt > 1 && !o.ws_mt) {
       if (units < 8 * sms) continue;
       const double rounds = std::ceil((double)units / sms), ideal = (double)units / sms;
       if (rounds > 1.06 * ideal) continue;
@@ -637,8 +640,8 @@ bool ws_plan(const Problem& pb, bool pair, WsPlan* w) {
   return false;
 }
 
-Status run_ws(const Problem& pb, const WsPlan& w, const void* a, const void* b, const void* seed, void* out,
-              const tzc_epilogue& ep, cudaStream_t stream) {
+Status run_ws(const Problem& pb, const WsPlan& w, const Options& o, const void* a, const void* b, const void* seed,
+              void* out, const tzc_epilogue& ep, cudaStream_t stream) {
   const int e = pb.f16 ? 2 : 1;
   const int KE = w.kb / e;
   const CUtensorMapDataType dt = pb.f16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_UINT8;
@@ -710,8 +713,8 @@ Status run_ws(const Problem& pb, const WsPlan& w, const void* a, const void* b, 
 #ifdef TZC_TRACE
   p.debug_flags = ::g_debug_flags;
 #endif
-  p.pol_a = (g_l2_hints & 1) ? tzcdev::kL2EvictFirst : 0;
-  p.pol_b = (g_l2_hints & 2) ? tzcdev::kL2EvictLast : 0;
+  p.pol_a = (o.l2_hints & 1) ? tzcdev::kL2EvictFirst : 0;
+  p.pol_b = (o.l2_hints & 2) ? tzcdev::kL2EvictLast : 0;
   p.magic_hw = ((uint64_t(1) << 40) + (uint64_t)pb.hp * pb.wp - 1) / ((uint64_t)pb.hp * pb.wp);
   p.magic_wp = ((uint64_t(1) << 40) + (uint64_t)pb.wp - 1) / (uint64_t)pb.wp;
   p.a_box_bytes = box_bytes;
@@ -721,9 +724,9 @@ Status run_ws(const Problem& pb, const WsPlan& w, const void* a, const void* b, 
   p.mt = w.mt;
   // as many accumulators as TMEM holds (<= 4): the epilogue may lag the MMAs
   // by NACC-1 units (the ping-pong epilogue groups need exactly 2)
-  p.nacc = g_ws_epi_groups == 2 ? 2 : std::min(4, 512 / (w.mt * w.bn));
-  p.epi_groups = g_ws_epi_groups;
-  fill_epilogue(&p, pb, seed, out, ep);
+  p.nacc = o.ws_epi_groups == 2 ? 2 : std::min(4, 512 / (w.mt * w.bn));
+  p.epi_groups = o.ws_epi_groups == 2 ? 2 : 1;
+  fill_epilogue(&p, pb, o, seed, out, ep);
   WsFn fn = ws_fn(w.bn, w.kb, pb.f16 != 0, w.pair != 0);
   if (!fn) return Status(TZC_E_INTERNAL, "no conv_ws instantiation");
   return fn(p, w.grid, w.smem, stream);
@@ -755,7 +758,8 @@ Problem s2d_problem(const Problem& pb) {
 }
 
 // Output layout, seed and fused-epilogue fields shared by both kernels.
-void fill_epilogue(ConvKernelParams* pp, const Problem& pb, const void* seed, void* out, const tzc_epilogue& ep) {
+void fill_epilogue(ConvKernelParams* pp, const Problem& pb, const Options& o, const void* seed, void* out,
+                   const tzc_epilogue& ep) {
   ConvKernelParams& p = *pp;
   p.out = out;
   p.seed = seed;
@@ -787,11 +791,11 @@ void fill_epilogue(ConvKernelParams* pp, const Problem& pb, const void* seed, vo
               pb.out.nb == pb.ngemm)
                  ? 1
                  : 0;
-  p.vec32 = (p.simple && g_st256 && pb.out.stride_m % 32 == 0 && reinterpret_cast<uintptr_t>(out) % 32 == 0) ? 1 : 0;
+  p.vec32 = (p.simple && o.st256 && pb.out.stride_m % 32 == 0 && reinterpret_cast<uintptr_t>(out) % 32 == 0) ? 1 : 0;
   {
     const int eo = (ep.kind == tzcdev::EP_REQUANT_I8) ? 1 : (ep.kind == tzcdev::EP_CAST_F16) ? 2 : 4;
     auto al32 = [eo](int64_t elems) { return (elems * eo) % 32 == 0; };
-    p.st32 = (g_st256 && eo > 1 && p.vec_ok && al32(pb.out.stride_m) && al32(pb.out.stride_blk) && al32(pb.out.nb) &&
+    p.st32 = (o.st256 && eo > 1 && p.vec_ok && al32(pb.out.stride_m) && al32(pb.out.stride_blk) && al32(pb.out.nb) &&
               reinterpret_cast<uintptr_t>(out) % 32 == 0)
                  ? 1
                  : 0;
@@ -799,35 +803,28 @@ void fill_epilogue(ConvKernelParams* pp, const Problem& pb, const void* seed, vo
 }
 
 // ---- launch --------------------------------------------------------------------
-Status run_problem(const Problem& pb, const void* a, const void* b, const void* seed, void* out,
+Status run_problem(const Problem& pb, const Options& o, const void* a, const void* b, const void* seed, void* out,
                    const tzc_epilogue& ep, cudaStream_t stream) {
   if (!device_ok()) return Status(TZC_E_DEVICE, "no usable sm_100 (B200) device");
   Status st = load_driver();
   if (!st.ok()) return st;
-  static const bool env_no_ws = [] {
-    if (std::getenv("TZC_B200_NO_WS")) g_ws_enabled = 0;
-    return true;
-  }();
-  (void)env_no_ws;
-  if (needs_k7(pb) && s2d_eligible(pb)) {
-    // the stem: space-to-depth to 16-byte pixels, then the shifted-window
-    // kernel in pair mode (two taps per K=32 MMA)
-    const Problem q = s2d_problem(pb);
+  {
+    bool s2d = false;
+    Problem q;
     WsPlan w;
-    if (ws_plan(q, !pb.f16, &w)) {
+    if (ws_route(pb, o, &q, &w, &s2d)) {
+      if (!s2d) return run_ws(pb, w, o, a, b, seed, out, ep, stream);
+      // the stem: space-to-depth to 16-byte pixels, then the shifted-window
+      // kernel in pair mode (two taps per K=32 MMA)
       void* x4 = nullptr;
       void* w4 = nullptr;
       const int eb = pb.f16 ? 2 : 1;
       st = workspace(1, (size_t)(((int64_t)q.n * q.hp * q.wp + 7) / 8 * 8) * 16 * eb, &x4, stream);
       if (st.ok()) st = workspace(2, (size_t)q.ngemm * q.taps * 16 * eb, &w4, stream);
       if (st.ok()) st = s2d_stem(pb, a, b, x4, w4, q.hp, q.wp, q.r, q.s, stream);
-      if (st.ok()) st = run_ws(q, w, x4, w4, seed, out, ep, stream);
+      if (st.ok()) st = run_ws(q, w, o, x4, w4, seed, out, ep, stream);
       return st;
     }
-  }
-  if (!needs_k7(pb)) {
-    WsPlan w;
-    if (g_ws_enabled && ws_plan(pb, false, &w)) return run_ws(pb, w, a, b, seed, out, ep, stream);
   }
   if (needs_k7(pb)) {
     // K7: channel runs too thin for TMA (the C=3 stem).  Materialise
@@ -842,10 +839,10 @@ Status run_problem(const Problem& pb, const void* a, const void* b, const void* 
     if (st.ok()) st = im2col_pad(pb, a, wa, kp, stream);
     if (st.ok()) st = weight_pad(pb, b, wb, kp, stream);
     if (!st.ok()) return st;
-    return run_problem(g, wa, wb, seed, out, ep, stream);
+    return run_problem(g, o, wa, wb, seed, out, ep, stream);
   }
   tzc_plan plan;
-  st = plan_problem(pb, &plan);
+  st = plan_problem(pb, o, &plan);
   if (!st.ok()) return st;
   const int e = pb.f16 ? 2 : 1;
   const int KE = plan.bk_bytes / e;
@@ -856,8 +853,8 @@ Status run_problem(const Problem& pb, const void* a, const void* b, const void* 
 #ifdef TZC_TRACE
   p.debug_flags = ::g_debug_flags;
 #endif
-  p.pol_a = (g_l2_hints & 1) ? tzcdev::kL2EvictFirst : 0;
-  p.pol_b = (g_l2_hints & 2) ? tzcdev::kL2EvictLast : 0;
+  p.pol_a = (o.l2_hints & 1) ? tzcdev::kL2EvictFirst : 0;
+  p.pol_b = (o.l2_hints & 2) ? tzcdev::kL2EvictLast : 0;
   // ---- A operand
   if (pb.a_mode == tzcdev::A_TILED) {
     cuuint64_t dims[2] = {(cuuint64_t)pb.a_kdim, (cuuint64_t)pb.a_rows};
@@ -923,23 +920,23 @@ Status run_problem(const Problem& pb, const void* a, const void* b, const void* 
   p.splits = plan.splits;
   {
     const WorkSplit wsplit = work_split(p.num_tiles, plan.tiles_n, p.num_kb, num_sms(), pb.ngemm % 16 == 0,
-                                        pb.forced_splits ? pb.forced_splits : g_forced_splits);
+                                        pb.forced_splits ? pb.forced_splits : o.splits, o);
     p.full_units = wsplit.full;
     p.red_m0 = (int32_t)((wsplit.full / plan.tiles_n) * 128);
     p.red_rows = (int32_t)(pb.m - p.red_m0);
   }
   p.stages = plan.stages;
-  p.epi_groups = epi_groups_for(p.num_kb / plan.splits);
+  p.epi_groups = epi_groups_for(p.num_kb / plan.splits, o);
   p.fd_splits = make_fdiv(plan.splits);
   p.fd_tiles_n = make_fdiv(plan.tiles_n);
   p.fd_ohow = make_fdiv(std::max<int64_t>(1, (int64_t)pb.oh * pb.ow));
   p.fd_ow = make_fdiv(std::max(1, pb.ow));
   p.fd_cblocks = make_fdiv(std::max(1, p.c_blocks));
   p.fd_s = make_fdiv(std::max(1, pb.s));
-  fill_epilogue(&p, pb, seed, out, ep);
+  fill_epilogue(&p, pb, o, seed, out, ep);
   if (ep.kind == tzcdev::EP_REQUANT_I8 && p.full_units > 0 && p.vec_ok && pb.out.nb == pb.ngemm &&
       pb.out.stride_m == pb.ngemm && pb.ngemm % plan.bn == 0 &&
-      (g_tma_store == 1 || (g_tma_store == 2 && (int64_t)p.num_kb * plan.bk_bytes <= g_tma_store_k))) {
+      (o.tma_store == 1 || (o.tma_store == 2 && (int64_t)p.num_kb * plan.bk_bytes <= o.tma_store_k))) {
     // int8 output as a [M, Ngemm] map; one box = 32 rows x min(BN, 128) bytes
     const int rb = std::min(plan.bn, 128);
     cuuint64_t dims[2] = {(cuuint64_t)pb.ngemm, (cuuint64_t)pb.m};
@@ -956,8 +953,8 @@ Status run_problem(const Problem& pb, const void* a, const void* b, const void* 
   }
   // without the TMA-store staging tiles the ring gets their SMEM
   if (!p.tma_store) p.stages = ring_stages(plan.bn, plan.bk_bytes, 0);
-  if (g_pair && ep.kind == tzcdev::EP_REQUANT_I8 && p.vec_ok && pb.ngemm % plan.bn == 0 && !pb.f16 && !pb.b_kn &&
-      plan.splits == 1 && p.full_units == p.num_tiles && p.num_kb >= g_pair_min_kb &&
+  if (o.pair && ep.kind == tzcdev::EP_REQUANT_I8 && p.vec_ok && pb.ngemm % plan.bn == 0 && !pb.f16 && !pb.b_kn &&
+      plan.splits == 1 && p.full_units == p.num_tiles && p.num_kb >= o.pair_min_kb &&
       p.epi_groups == 1 && plan.bk_bytes == 128 && (plan.bn == 128 || plan.bn == 256) &&
       (pb.a_mode == tzcdev::A_TILED || pb.a_mode == tzcdev::A_IM2COL) && num_sms() >= 2) {
     // CTA pairs: 256-row tiles, each CTA loads its A rows and half the B rows

@@ -6,6 +6,8 @@
 #include <atomic>
 #include <cstdint>
 #include <string>
+#include <utility>
+#include <vector>
 
 #include "tzc_b200.h"
 
@@ -38,27 +40,46 @@ struct Problem {
   int forced_splits = 0;
 };
 
-Status plan_problem(const Problem& pb, tzc_plan* plan);
+// Plan knobs, named as tzc_b200_set_option names them.  Every launch plans
+// from one snapshot (the process defaults plus the per-descriptor overrides
+// the tuner installs), taken once per call and passed down by value, so a
+// concurrent set_option never changes a plan half-way through a call.
+// Options choose the kernel plan only, never the results.
+struct Options {
+  int splits = 0;               // forced split-K factor (0 = automatic)
+  int shifted_window = 1;       // weight-stationary kernel for eligible stride-1 convs
+  int ws_epi_groups = 1;        // shifted window: 1 or 2 (ping-pong) epilogue groups
+  int tail_split = 0;           // split the under-filled last round of tiles along K
+  int split_min_kb = 1 << 20;   // automatic split-K keeps >= this many K blocks per split (off)
+  int pingpong_kb = 2;          // general kernel: ping-pong epilogue groups up to this many K blocks
+  int ws_mt = 0;                // shifted window: force 1/2/4 tiles per work unit (0 = automatic)
+  int ws_1x1_k = 64;            // shifted window for 1x1 convs with K <= this many bytes
+  int ws_1x1 = 0;               // ... for every 1x1 stride-1 conv
+  int bn = 0;                   // force the N tile (0 = automatic)
+  int tma_store_k = 64;         // tma_store == 2: TMA-store epilogue for GEMM K <= this many bytes
+  int pair_min_kb = 16;         // CTA pairs for layers with >= this many K blocks
+  int pair = 0;                 // CTA-pair (cta_group::2) kernel for eligible int8 layers
+  int st256 = 1;                // 256-bit epilogue stores where aligned
+  int l2_hints = 1;             // 1: A loads evict-first; 2: B loads evict-last
+  int tma_store = 0;            // int8 TMA-store epilogue: 0 never, 1 always, 2 by K
+};
+// Validates and applies one named option; false (with *err) for an unknown
+// name or an illegal value.
+bool apply_option(Options* o, const std::string& name, int64_t value, std::string* err);
+const char* const* option_names();  // null-terminated
+// Snapshot of the process defaults (tzc_b200_set_option) plus the overrides
+// installed for `key` (a descriptor's bytes; "" = none).
+Options options_for(const std::string& key);
+Status parse_option_spec(const std::string& spec, Options* o, std::vector<std::pair<std::string, int64_t>>* items);
+Status set_default_option(const std::string& name, int64_t value);
+Status set_problem_options(const std::string& key, const std::string& spec);
+void clear_problem_options();
+
+Status plan_problem(const Problem& pb, const Options& o, tzc_plan* plan);
 bool needs_k7(const Problem& pb);
 Problem k7_gemm(const Problem& pb, int* kp_out);
-Status run_problem(const Problem& pb, const void* a, const void* b, const void* seed, void* out,
+Status run_problem(const Problem& pb, const Options& o, const void* a, const void* b, const void* seed, void* out,
                    const tzc_epilogue& ep, cudaStream_t stream);
-void set_forced_splits(int s);
-void set_ws_enabled(int on);
-void set_tma_store(int on);
-void set_tma_store_k(int k);
-void set_l2_hints(int h);
-void set_st256(int on);
-void set_pair(int on);
-void set_pair_min_kb(int kb);
-void set_forced_bn(int bn);
-void set_ws_1x1(int on);
-void set_ws_1x1_k(int k);
-void set_ws_mt(int mt);
-void set_pingpong_kb(int kb);
-void set_split_min_kb(int kb);
-void set_tail_split(int on);
-void set_ws_epi_groups(int g);
 int device_ok();
 int num_sms();
 
