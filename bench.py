@@ -49,6 +49,11 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--batch", type=int, default=256, help="global batch, sharded over the ranks")
+    ap.add_argument("--workload", default="resnet50", choices=["resnet50", "gemm4096", "c1"],
+                    help="resnet50: the BASELINE metric (configs[4], default); gemm4096: configs[1]; c1: configs[0]")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="process-group backend for the max-over-ranks reduction (gloo: CPU tensors; lets a "
+                         "test run two ranks on one GPU)")
     ap.add_argument("--layers", default="", help="comma list of layer names (default: all 23)")
     ap.add_argument("--profile", default="i8", choices=["i8", "f16"],
                     help="i8: the BASELINE metric (default); f16: configs[3] (fp16 in, fp32 accumulate, fp16 out)")
@@ -77,6 +82,8 @@ def max_over_ranks(x: float, world: int, device) -> float:
         return float(x)
     import torch
     import torch.distributed as dist
+    if dist.get_backend() == "gloo":  # gloo reduces CPU tensors
+        device = "cpu"
     t = torch.tensor([float(x)], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
@@ -334,6 +341,7 @@ def run_ours(args, rank, world, local):
     from paper_2101_08458_b200 import device as D
     from paper_2101_08458_b200._capi import lib
 
+    local = local % max(1, torch.cuda.device_count())  # more ranks than GPUs (tests): ranks share a device
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     assert lib().tzc_b200_device_ok() == 1, "libtzc_b200: no sm_100 device"
@@ -480,6 +488,10 @@ def run_ours(args, rank, world, local):
     torch.cuda.synchronize()
     launches_per_step = D.launch_count() - c0
     total_ms = max_over_ranks(sum(step_ms), world, dev)
+    per_rank = [sum(step_ms)]
+    if world > 1:
+        per_rank = [None] * world
+        dist.all_gather_object(per_rank, sum(step_ms))
     ms_step = total_ms / args.steps
     value = job_tops(ops_step, world, ms_step)  # TOPS, whole job
 
@@ -524,6 +536,7 @@ def run_ours(args, rank, world, local):
         "pct_of_spec_peak": round(100.0 * value / (spec * world), 2),
         "gpu_launches": launches_per_step * args.steps,
         "parity": parity,
+        "per_rank_ms_per_step": [round(t / args.steps, 4) for t in per_rank],
         "clocks": clk.summary(),
     }
     kern_ms = sum(statistics.median(v) for v in per_layer)  # per-layer event sum (graph B)
@@ -764,6 +777,8 @@ def cpu_baseline(seconds, layers):
 def run_reference(args, rank, world):
     if rank != 0:
         return
+    if args.workload != "resnet50":
+        return run_reference_op(args, world)
     from paper_2101_08458_b200.workloads import RESNET50_V15
     names = [s for s in args.layers.split(",") if s]
     layers = [L for L in RESNET50_V15 if not names or L.name in names]
@@ -795,6 +810,252 @@ def run_reference(args, rank, world):
     print(json.dumps(res))
 
 
+# ---------------------------------------------------------------------------
+# configs[1] / configs[0] as their own bench lines (--workload gemm4096 | c1)
+WL_METRIC = {
+    "gemm4096": "int8 Matmul 4096x4096x4096 (int32 accumulation, fused requant to int8) TOPS & % tcgen05 i8 peak",
+    "c1": "int8 Conv2D 3x3 56x56x64->64 batch 1 (the reference's own blocked lowering) TOPS",
+}
+
+
+def run_workload(args, rank, world, local):
+    """One tensorized op per step, device-resident inputs, L2 flushed between
+    steps (outside the timed events), one CUDA-graph replay per step timed with
+    CUDA events on the launching stream; max over ranks.
+
+    gemm4096: BASELINE configs[1], matmul_tdsl(4096,4096,4096) (A u8 [M,K],
+      B i8 [N,K], /root/reference/proj/src/workloads.cpp:41-63) with the
+      requant op Q = cast<i8>(cast<fp32>(C) * 2^-14) fused; rows sharded over
+      the ranks (strong scaling).
+    c1: BASELINE configs[0], conv2d_tdsl({64,56,64,3,1},16,4) exactly as the
+      reference lowers it (channel-blocked data [16,56,56,4], kernel
+      [4,16,3,3,16,4], int32 accumulate into the seeded blocked output
+      [4,54,54,16]; proj/src/workloads.cpp:65-92): the K5 unblock adapters
+      plus the tcgen05 conv with the blocked output layout.  Batch 1 does not
+      shard: N ranks run N replicas (weak)."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from paper_2101_08458_b200 import device as D
+    from paper_2101_08458_b200 import ops
+    from paper_2101_08458_b200._capi import lib
+    from paper_2101_08458_b200.workloads import conv2d_tdsl, matmul_tdsl, requant_tdsl
+
+    local = local % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    assert lib().tzc_b200_device_ok() == 1, "libtzc_b200: no sm_100 device"
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(77 + rank)
+    stream = torch.cuda.Stream(device=dev)
+    flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device=dev)
+    pk = peaks()
+    wl = args.workload
+    if wl == "gemm4096":
+        M = N = K = 4096
+        m = shard_batch(M, world)
+        scale = 2.0 ** -14
+        A = torch.randint(0, 256, (m, K), dtype=torch.uint8, device=dev, generator=gen)
+        B = torch.randint(-128, 128, (N, K), dtype=torch.int8, device=dev, generator=gen)
+        out = torch.empty((m, N), dtype=torch.int8, device=dev)
+        ops_step = 2 * m * N * K
+        algo_bytes = m * K + N * K + m * N
+
+        def launch():
+            D.gemm(A, B, None, epilogue="requant_i8", scale=scale, out=out, stream=stream)
+
+        def check():
+            from oracle.pyoracle import Orc
+            An, Bn = A.cpu().numpy(), B.cpu().numpy()
+            rows = np.unique(np.r_[0, m - 1, np.random.default_rng(rank).choice(m, 30, replace=False)])
+            want = Orc.requant_i8(Orc.matmul(An[rows], Bn), scale)
+            return bool(np.array_equal(out.cpu().numpy()[rows], want)), f"{len(rows)} whole rows (first, last, 30 random)"
+
+        text = matmul_tdsl(m, N, K)
+        host_in = {"A": A.cpu().numpy(), "B": B.cpu().numpy()}
+        ep_text = requant_tdsl((m, N), scale, src="C")
+        instr = "tcgen05_i8_m128n256k32"
+        workload = "matmul_tdsl(4096,4096,4096) + requant (configs[1])"
+        from paper_2101_08458_b200._capi import GemmDesc
+        gd = GemmDesc(profile=0, m=m, n=N, k=K, b_kn=0)
+        gd.out = D.nhwc_layout(N)
+        plan = D.plan_gemm(gd)
+    else:
+        c, hw, k, r, cb, kb = 64, 56, 64, 3, 4, 16
+        o = hw - r + 1
+        data = torch.randint(0, 256, (c // cb, hw, hw, cb), dtype=torch.uint8, device=dev, generator=gen)
+        kern = torch.randint(-128, 128, (k // kb, c // cb, r, r, kb, cb), dtype=torch.int8, device=dev, generator=gen)
+        seed = torch.randint(-(2 ** 31), 2 ** 31, (k // kb, o, o, kb), dtype=torch.int32, device=dev, generator=gen)
+        out = torch.empty((k // kb, o, o, kb), dtype=torch.int32, device=dev)
+        x = torch.empty((1, hw, hw, c), dtype=torch.uint8, device=dev)
+        w = torch.empty((k, r, r, c), dtype=torch.int8, device=dev)
+        lay = D.blocked_layout(k, o * o, kb)
+        ops_step = 2 * o * o * k * c * r * r
+        algo_bytes = hw * hw * c + k * r * r * c + 2 * 4 * o * o * k  # seed read + int32 out
+
+        def launch():
+            from paper_2101_08458_b200._capi import check as ck
+            L_ = lib()
+            ck(L_.tzc_b200_unblock_data(C.c_void_p(data.data_ptr()), C.c_void_p(x.data_ptr()), c, hw, hw, cb, 1,
+                                        C.c_void_p(stream.cuda_stream)))
+            ck(L_.tzc_b200_unblock_kernel(C.c_void_p(kern.data_ptr()), C.c_void_p(w.data_ptr()), k, c, r, r, kb, cb, 1,
+                                          C.c_void_p(stream.cuda_stream)))
+            D.conv2d(x, w, 1, seed, out=out, out_layout=lay, stream=stream)
+
+        text = conv2d_tdsl(c, hw, k, r, 1, kb, cb)
+
+        def check():
+            from oracle.pyoracle import Orc
+            ins = {"data": data.cpu().numpy(), "kernel": kern.cpu().numpy(), "out": seed.cpu().numpy()}
+            want = Orc.conv2d_blocked(ins["data"], ins["kernel"], 1, ins["out"])
+            return bool(np.array_equal(out.cpu().numpy(), want)), "the whole output (186 624 int32)"
+
+        host_in = {"data": data.cpu().numpy(), "kernel": kern.cpu().numpy(), "out": seed.cpu().numpy()}
+        ep_text = None
+        instr = "tcgen05_i8_m128n64k32"
+        workload = "conv2d_tdsl({64,56,64,3,1},16,4), blocked layouts, seeded int32 output (configs[0])"
+        plan = {}
+
+    with torch.cuda.stream(stream):
+        launch()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=stream):
+        launch()
+    torch.cuda.synchronize()
+    out.zero_()
+    torch.cuda.synchronize()
+    with torch.cuda.stream(stream):
+        g.replay()
+    torch.cuda.synchronize()
+    ok, what = check()
+    if not ok:
+        raise SystemExit(f"parity gate: {wl}: output differs from the oracle ({what})")
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+    def step():
+        flush.zero_()
+        torch.cuda.synchronize()
+        with torch.cuda.stream(stream):
+            e0.record(stream)
+            g.replay()
+            e1.record(stream)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1)
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    if world > 1:
+        dist.barrier()
+    ts = []
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            ts.append(step())
+    torch.cuda.synchronize()
+    total = max_over_ranks(sum(ts), world, dev)
+    ms = total / args.steps
+    value = ops_step * world / (ms * 1e-3) / 1e12
+    kern_ms = statistics.median(ts)
+    c0 = D.launch_count()
+    with torch.cuda.stream(stream):
+        launch()
+    torch.cuda.synchronize()
+    launches = D.launch_count() - c0
+
+    # e2e: the reference-facing op call with host buffers (H2D + kernel + D2H timed)
+    hout = np.empty(tuple(out.shape), dtype=np.int8 if wl == "gemm4096" else np.int32)
+    pinned = {kk: torch.from_numpy(v).pin_memory().numpy() for kk, v in host_in.items()}
+    hout_p = torch.empty(hout.shape, dtype=torch.int8 if wl == "gemm4096" else torch.int32).pin_memory().numpy()
+    for _ in range(2):
+        ops.run_op(text, instr, pinned, epilogue=ep_text, out=hout_p)
+    if not np.array_equal(hout_p, out.cpu().numpy()):
+        raise SystemExit(f"e2e parity: {wl}: run_op output differs from the device path")
+    t0 = time.perf_counter()
+    n_e2e = max(3, min(args.steps, 10))
+    for _ in range(n_e2e):
+        ops.run_op(text, instr, pinned, epilogue=ep_text, out=hout_p)
+    e2e_ms = max_over_ranks((time.perf_counter() - t0) * 1e3, world, dev) / n_e2e
+    h2d = sum(v.nbytes for v in pinned.values())
+
+    tpeak = pk["i8_tops"]
+    ach = ops_step / (kern_ms * 1e-3) / 1e12
+    res = {
+        "metric": WL_METRIC[wl], "value": round(value, 3), "unit": "TOPS", "n_gpus": world, "steps": args.steps,
+        "warmup": max(3, args.warmup), "ms_per_step": round(ms, 5), "higher_is_better": True,
+        "scaling": "strong" if wl == "gemm4096" else "weak", "vs_baseline": None, "dtype": "u8xi8->i32",
+        "data": "synthetic (uniform u8 / i8, torch.Generator seeded per rank)",
+        "config": {"workload": workload, "parallelism": f"dp{world}" + (" (rows sharded)" if wl == "gemm4096" else
+                                                                        " (replicas)"),
+                   "l2": "flushed (512 MiB memset) between timed steps, outside the timed events",
+                   "plan": plan},
+        "pct_of_spec_peak": round(100.0 * value / (SPEC_I8_TOPS * world), 2),
+        "gpu_launches": launches * args.steps,
+        "parity": {"bitexact": True, "checked": what, "after": "one replay of the timed graph"},
+        "clocks": clk.summary(),
+        "roofline": {"bound": "tensor", "kernel": "conv_tc_kernel (tcgen05 kind::i8)" if wl == "gemm4096" else
+                     "K5 unblock + conv kernel (launch-latency bound at batch 1)",
+                     "achieved": round(ach, 2), "peak": round(tpeak, 1), "unit": "TFLOP/s",
+                     "frac": round(ach / tpeak, 4), "frac_of_spec": round(ach / SPEC_I8_TOPS, 4),
+                     "peak_basis": f"2 x bf16 burst, {pk['source']}; spec dense i8 = {SPEC_I8_TOPS}",
+                     "algorithmic_per_launch": {"ops": ops_step, "bytes": algo_bytes},
+                     "traffic": None},
+        "e2e": {"value": round(ops_step * world / (e2e_ms * 1e-3) / 1e12, 4), "unit": "TOPS",
+                "ms_per_step": round(e2e_ms, 3), "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": hout_p.nbytes,
+                "path": "tzc_b200_run_op (op text + tcgen05 instruction + pinned host buffers), host wall clock"},
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        res["cpu_baseline"] = cpu_baseline_op(args.cpu_seconds, wl)
+    if rank == 0:
+        print(json.dumps(res))
+
+
+def cpu_sample_items(wl, budget_macs):
+    """Bounded slices of the workload's own op for the reference CPU path."""
+    from paper_2101_08458_b200.workloads import conv2d_tdsl, matmul_tdsl
+    if wl == "gemm4096":
+        n = max(16, min(4096, int(budget_macs / 4096) // 16 * 16))
+        return [("gemm rows", matmul_tdsl(1, n, 4096), n * 4096, True)]
+    # c1: the reference's own op at full size is 107.5 M MAC (60 s on the VM);
+    # a K-slice of it (16 of 64 output channels) keeps the same lowering
+    return [("c1 slice", conv2d_tdsl(64, 56, 16, 3, 1, 16, 4), 54 * 54 * 16 * 64 * 9, True)]
+
+
+def cpu_baseline_op(seconds, wl):
+    threads = os.cpu_count() or 1
+    items = cpu_sample_items(wl, seconds * 0.8e6)
+    items = items * threads
+    macs, dt = run_cpu_sample(items, threads)
+    return {"value": round(2 * macs / dt / 1e12, 9), "unit": "TOPS", "cores": threads, "kind": "reference",
+            "seconds": round(dt, 2),
+            "sample": f"{len(items)} copies of {items[0][0]} ({items[0][2]} MAC each); eval_tir(vdot_16x4), "
+                      "oracle/_ref/libtzc_ref.so built from /root/reference"}
+
+
+def run_reference_op(args, world):
+    """--impl reference --workload gemm4096|c1: the reference's eval_tir(vdot_16x4)
+    on bounded slices of the same op, every host thread."""
+    threads = os.cpu_count() or 1
+    budget = max(1.0, min(args.cpu_seconds, 150.0 / max(1, args.steps + args.warmup)))
+    items = cpu_sample_items(args.workload, budget * 0.8e6) * threads
+    for _ in range(args.warmup):
+        run_cpu_sample(items, threads)
+    tot_macs, tot_s = 0, 0.0
+    for _ in range(args.steps):
+        m, s_ = run_cpu_sample(items, threads)
+        tot_macs += m
+        tot_s += s_
+    value = 2 * tot_macs / tot_s / 1e12
+    print(json.dumps({
+        "metric": WL_METRIC[args.workload], "value": round(value, 9), "unit": "TOPS", "impl": "reference",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(1e3 * tot_s / args.steps, 2), "higher_is_better": True,
+        "scaling": "strong" if args.workload == "gemm4096" else "weak", "vs_baseline": None, "dtype": "u8xi8->i32",
+        "data": "synthetic (reference random_inputs, seed 0)", "config": {"workload": args.workload},
+        "cpu_baseline": {"value": round(value, 9), "unit": "TOPS", "cores": threads, "kind": "reference",
+                         "sample": f"per step {len(items)} x {items[0][0]} ({items[0][2]} MAC); eval_tir(vdot_16x4)"},
+        "e2e": {"value": round(value, 9), "unit": "TOPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
+
+
 def main():
     args = parse()
     rank, world, local = dist_env()
@@ -803,9 +1064,12 @@ def main():
         return
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl")
+        dist.init_process_group(args.dist_backend)
     try:
-        run_ours(args, rank, world, local)
+        if args.workload == "resnet50":
+            run_ours(args, rank, world, local)
+        else:
+            run_workload(args, rank, world, local)
     finally:
         if world > 1:
             import torch.distributed as dist

@@ -37,6 +37,7 @@
 #include <optional>
 #include <stdexcept>
 #include <string>
+#include <tuple>
 #include <vector>
 
 #if defined(__GNUC__)
@@ -287,17 +288,51 @@ struct KernelPlan {
   int64_t dp = 1, kd = 1, od = 1; // ConvBlocked3D: input depth, depth taps, output depth
   std::string describe() const;
 };
-struct TensorizedOp {
-  ComputeOp op;
-  LoopMapping mapping;
-  std::vector<std::string> schedule;  // split / reorder / pragma lines (reference schedule text)
-  std::vector<std::string> outer_dp, outer_red, pragma_axes;
-  KernelPlan plan;
+struct Transform;
+using Schedule = std::vector<Transform>;
+// ============================ schedules ==================================
+// (declared ahead of TensorizedOp, which carries one)
+struct Transform {
+  enum class Kind : uint8_t { Pad, Split, Reorder, Fuse, Parallel, Unroll, SplitReduction, Pragma };
+  Kind kind = Kind::Split;
+  std::string a, b;
+  std::vector<std::string> names;
+  int64_t factor = 0;
+  static std::string kind_name(Kind k);
 };
-// Throws DivisibilityError only when padding is not allowed and the device
-// cannot cover a tail; InjectError when the op's layout has no kernel.
+std::string print_schedule(const Schedule& s);     // one transform per line
+Schedule parse_schedule(const std::string& text);  // SyntaxError on bad lines
+Schedule load_schedule(const std::string& path);   // IoError when unreadable
+
+// The reference's pad_to_multiple (proj/include/tzc/rewriter.hpp:44-49):
+// raises `loop` to the next multiple of `multiple`, growing every tensor
+// dimension it indexes (zero extension).  A reduction loop may only be
+// padded when a multiplicative factor of the reduction term reads a
+// zero-extended index for every added iteration; otherwise PadUnsupported.
+// On the device the zero extension is TMA out-of-bounds fill, not a copy.
+ComputeOp pad_to_multiple(const ComputeOp& op, const std::string& loop, int64_t multiple);
+
+// The reference's TensorizedOp (proj/include/tzc/rewriter.hpp:56-65) plus the
+// device plan this backend executes.
+struct TensorizedOp {
+  ComputeOp op;        // possibly padded
+  ComputeOp original;  // before padding (equal to op when nothing was padded)
+  LoopMapping mapping;
+  Schedule schedule;   // pads + (fuses) + splits + reorder + pragma
+  std::vector<std::string> outer_dp, outer_red, pragma_axes;
+  // Backend: the sm_100a kernel realising the pragma nest; has_plan is false
+  // for instructions this backend does not execute (the CPU descriptions).
+  KernelPlan plan;
+  bool has_plan = false;
+};
+// Pure schedule construction for any instruction, as in the reference:
+// DivisibilityError when a mapped extent is not a multiple of its instruction
+// extent and allow_pad is false (the reference default).  For tcgen05
+// instructions the device plan is derived too (InjectError when the op's
+// layout has no sm_100a kernel); fused pixel groups (F6) are split with
+// device-clipped tails instead of padded.
 TensorizedOp tile_and_reorder(const ComputeOp& op, const Intrinsic& intr, const LoopMapping& mapping,
-                              bool allow_pad = true);
+                              bool allow_pad = false);
 // Convenience: match, pick the first device-realisable mapping, tile.
 TensorizedOp tensorize(const ComputeOp& op, const Intrinsic& intr);
 
@@ -307,19 +342,6 @@ TensorizedOp tensorize(const ComputeOp& op, const Intrinsic& intr);
 // the imperative TensorIR nest; inject_intrinsic replaces its tensorize
 // pragma nest with one instruction call; eval_tir executes it — here on the
 // B200 only (tcgen05 descriptions), never on a CPU interpreter.
-struct Transform {
-  enum class Kind : uint8_t { Pad, Split, Reorder, Fuse, Parallel, Unroll, SplitReduction, Pragma };
-  Kind kind = Kind::Split;
-  std::string a, b;
-  std::vector<std::string> names;
-  int64_t factor = 0;
-  static std::string kind_name(Kind k);
-};
-using Schedule = std::vector<Transform>;
-std::string print_schedule(const Schedule& s);     // one transform per line
-Schedule parse_schedule(const std::string& text);  // SyntaxError on bad lines
-Schedule load_schedule(const std::string& path);   // IoError when unreadable
-
 enum class LoopAnn : uint8_t { Serial, Parallel, Unrolled, Tensorize };
 std::string loop_ann_name(LoopAnn a);
 
@@ -377,10 +399,9 @@ struct LowerOptions {
   // stores).  tensorized_ir sets it for fused pixel groups (F6).
   bool clip_tails = false;
 };
-// Pad transforms throw PadUnsupported: this backend realises padding with
-// TMA out-of-bounds zero fill inside the kernel (tile_and_reorder's plan).
+// Leading Pad transforms reshape the op (pad_to_multiple), the rest works on
+// axes — the reference's lower (proj/src/rewriter.cpp:509-646).
 TensorIR lower(const ComputeOp& op, const Schedule& schedule, const LowerOptions& opts = {});
-TensorIR lower(const ComputeOp& op, const std::vector<std::string>& schedule_lines, const LowerOptions& opts = {});
 TensorIR inject_intrinsic(const TensorIR& ir, const Intrinsic& intr, const LoopMapping& mapping);
 // lower(tile_and_reorder schedule) + inject for the first device-realisable mapping.
 TensorIR tensorized_ir(const ComputeOp& op, const Intrinsic& intr);
@@ -416,6 +437,40 @@ void save_tensor(const std::string& path, const TensorValue& v);
 TensorValue load_tensor(const std::string& path);
 std::string tensor_to_text(const TensorValue& v, int64_t max_elems = 64);
 
+// Zero-extends `v` into `shape` / slices the leading region back out (the
+// reference's embed / slice, proj/include/tzc/vm.hpp:103-106; host helpers
+// around padded pipelines).
+TensorValue embed(const TensorValue& v, const std::vector<int64_t>& shape);
+TensorValue slice(const TensorValue& v, const std::vector<int64_t>& shape);
+
+// ============================ cost ledger ================================
+// The reference's operation counters (proj/include/tzc/vm.hpp:62-99).  They
+// are pure functions of the nest's loop extents (no data-dependent control
+// flow), so both entry points compute them without evaluating any tensor
+// value: measure_static from the extents, measure by walking the executed
+// iteration space.  On this backend they describe the nest (work
+// conservation, tuner ranking on the reference's CPU sketches); device time
+// comes from CUDA events (tzc_b200_tune_*).
+struct CostReport {
+  int64_t scalar_mac_count = 0;  // executed scalar stores weighted by their value's Mul count
+  int64_t load_count = 0;        // scalar loads + gathered vector lanes
+  int64_t store_count = 0;       // scalar stores + scattered vector lanes
+  std::map<std::string, int64_t> intrinsic_calls;
+  int64_t intrinsic_call_count = 0;
+  int64_t parallel_credit = 1;   // max parallel loop extent
+  int64_t unroll_depth = 1;      // product of unrolled loop extents
+  std::string to_string() const;
+};
+CostReport measure(const TensorIR& ir, const Inputs& inputs);
+CostReport measure_static(const TensorIR& ir);
+struct CostModel {
+  int64_t cores = 24;
+  int64_t unroll_target = 4;
+};
+using CostKey = std::tuple<int64_t, int64_t, int64_t>;
+CostKey cost_key(const CostReport& r, const CostModel& m = {});
+std::string cost_key_to_string(const CostKey& k);
+
 // Executes a tensorized op on the B200 (the role eval_tir plays on the
 // reference VM).  Inputs as for eval_tir: declared inputs plus, for
 // accumulate-form ops, the output's initial image under the output's name.
@@ -439,6 +494,112 @@ TensorizedOp device_plan(const TensorIR& ir);
 // declared element width, row-major.
 void run_tensorized_packed(const TensorizedOp& t, const std::map<std::string, const void*>& host_inputs,
                            void* host_out, int64_t out_bytes, const ComputeOp* epilogue_op = nullptr);
+
+// ============================ workloads ==================================
+// The reference's generators and banks (proj/include/tzc/workloads.hpp:13-64):
+// surface .tdsl texts, channel-blocked data [C/cb,H,W,cb], kernel
+// [K/kb,C/cb,R,S,kb,cb], output [K/kb,OH,OW,kb]; valid convolutions.
+struct ConvShape {
+  std::string name;
+  int64_t in_c = 0;
+  int64_t in_hw = 0;
+  int64_t out_c = 0;
+  int64_t kernel = 0;
+  int64_t stride = 1;
+  int64_t out_hw() const { return (in_hw - kernel) / stride + 1; }
+};
+struct DtypeProfile {
+  DType data;
+  DType weight;
+  DType acc;
+};
+inline DtypeProfile int8_profile() { return {kU8, kI8, kI32}; }
+inline DtypeProfile fp16_profile() { return {kF16, kF16, kF32}; }
+std::string matmul_tdsl(int64_t m, int64_t n, int64_t k, const DtypeProfile& p = int8_profile());
+std::string conv2d_tdsl(const ConvShape& c, int64_t lane_block, int64_t red_block,
+                        const DtypeProfile& p = int8_profile());
+std::string conv3d_tdsl(const ConvShape& c, int64_t lane_block, int64_t red_block,
+                        const DtypeProfile& p = int8_profile());
+// Backend addition: batched NHWC (pre-padded) conv, [K,R,S,C] weights.
+std::string conv2d_nhwc_tdsl(int64_t n, int64_t hp, int64_t wp, int64_t c, int64_t k, int64_t r, int64_t s,
+                             int64_t stride = 1, const DtypeProfile& p = int8_profile());
+const std::vector<ConvShape>& table1_bank();
+const std::vector<ConvShape>& resnet18_3d_bank();
+// Backend addition: the 23 distinct ResNet-50 v1.5 convolutions (SURVEY.md
+// App. A) with the pad materialised in in_hw.
+const std::vector<ConvShape>& resnet50_bank();
+struct BankEntry {
+  ConvShape shape;
+  std::string tdsl;
+  bool is_3d = false;
+};
+// "table1" | "resnet18_3d" (| "resnet50": NHWC, batch 1); ShapeError otherwise.
+std::vector<BankEntry> bank_by_name(const std::string& name);
+
+// ============================ sketches + tuner ===========================
+// The reference's search API (proj/include/tzc/rewriter.hpp:100-131,
+// proj/include/tzc/tuner.hpp:12-72).  Target::Gpu runs the measured-time
+// search on the B200 for tcgen05 descriptions: every candidate device plan
+// (tile width, split-K = split_reduction, kernel family, tiles per unit,
+// epilogue grouping, CTA pairs) is timed with CUDA events and ranked by time;
+// CostKey = (median ns, 0, 0).  The CPU sketch space (threading / unrolling
+// for the reference's CPU VM) is out of scope for this backend
+// (SURVEY.md §2 row 7): its entry points throw InjectError.
+struct CpuSketch {
+  int l1 = 0;
+  int64_t f1 = 1;
+  int l2 = 0;
+  int64_t f2 = 1;
+  std::string to_string() const;
+};
+struct GpuSketch {
+  int64_t p = 1;
+  bool fuse_hw = false;
+  int64_t split_k = 1;
+  std::string to_string() const;
+};
+Schedule apply_cpu_sketch(const TensorizedOp& t, const CpuSketch& sketch);
+Schedule apply_gpu_sketch(const TensorizedOp& t, const GpuSketch& sketch);
+int64_t cpu_fused_parallel_extent(const TensorizedOp& t, const CpuSketch& s);
+int64_t cpu_unroll_factor(const TensorizedOp& t, const CpuSketch& s);
+struct CpuLimits {
+  int64_t parallel_bound = 3000;
+  int64_t unroll_bound = 8;
+};
+struct GpuLimits {
+  int64_t p_max = 2;
+  std::vector<int64_t> split_factors = {64};
+  bool allow_fuse = true;
+};
+std::vector<CpuSketch> enumerate_cpu_space(const TensorizedOp& t, const CpuLimits& limits = {});
+std::vector<GpuSketch> enumerate_gpu_space(const TensorizedOp& t, const GpuLimits& limits = {});
+enum class Target : uint8_t { Cpu, Gpu };
+struct TuneOptions {
+  Target target = Target::Cpu;
+  int budget = 16;
+  uint64_t seed = 0;
+  bool allow_pad = true;
+  CpuLimits cpu_limits{};
+  GpuLimits gpu_limits{};
+  CostModel cost_model{};
+  int64_t verify_limit = 1 << 22;
+  bool force_verify = false;
+  std::ostream* log = nullptr;
+};
+struct Candidate {
+  int id = -1;
+  LoopMapping mapping;
+  std::string sketch;
+  Schedule schedule;
+  CostReport cost;
+  CostKey key{};
+  bool verified = false;
+};
+struct TuneResult {
+  Candidate best;
+  std::vector<Candidate> evaluated;
+};
+TuneResult tune(const ComputeOp& op, const Intrinsic& intr, const TuneOptions& opts = {});
 
 }  // namespace tzc
 

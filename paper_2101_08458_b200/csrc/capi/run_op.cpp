@@ -119,7 +119,7 @@ extern "C" TZC_API int tzc_b200_describe(const char* op_tdsl, const char* intrin
   return guarded([&] {
     const tzc::TensorizedOp& t = *tensorized(op_tdsl, intrinsic);
     std::string s = "mapping " + t.mapping.to_string() + "\nplan " + t.plan.describe() + "\n";
-    for (const auto& l : t.schedule) s += l + "\n";
+    s += tzc::print_schedule(t.schedule);
     return put(s, buf, n);
   });
 }

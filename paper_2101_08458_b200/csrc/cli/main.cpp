@@ -165,7 +165,7 @@ int cmd_tensorize(const Args& a, std::ostream& out) {
   if (!a.schedule_out.empty()) {
     std::ofstream f(a.schedule_out);
     if (!f) throw tzc::IoError("cannot open '" + a.schedule_out + "' for writing");
-    for (const auto& l : t.schedule) f << l << "\n";
+    f << tzc::print_schedule(t.schedule);
   }
   return 0;
 }

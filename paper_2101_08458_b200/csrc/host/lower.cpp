@@ -14,7 +14,9 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <map>
 #include <mutex>
+#include <set>
 #include <random>
 #include <sstream>
 
@@ -408,71 +410,131 @@ KernelPlan plan_for(const ComputeOp& op, const Intrinsic& intr, const LoopMappin
 
 }  // namespace
 
+static bool is_tcgen05(const Intrinsic& intr) { return intr.target_mnemonic.rfind("tcgen05.", 0) == 0; }
+
+// The reference's tensorize tiling (proj/include/tzc/rewriter.hpp:56-69):
+// pads (if allowed), one split per mapped loop by its instruction extent,
+// then a reorder putting the outer pieces (declaration order, data-parallel
+// before reduction) above the inner pieces (instruction loop order), which
+// the pragma tags.  Backend additions: a fused pixel group (F6) is fused
+// into one axis before its split; for tcgen05 instructions a non-dividing
+// extent is not padded in the op but clipped on the device (TMA
+// out-of-bounds zero fill / masked stores), and the kernel plan is derived.
 TensorizedOp tile_and_reorder(const ComputeOp& op, const Intrinsic& intr, const LoopMapping& mapping, bool allow_pad) {
-  MatchResult mr = match_operation(op, intr);
-  if (!mr.ok) throw InjectError("no structural match: " + mr.reason);
-  if (mapping.needs_padding && !allow_pad)
-    throw DivisibilityError("mapping " + mapping.to_string() + " needs padding (disallowed)");
+  const bool device = is_tcgen05(intr);
   TensorizedOp t;
-  t.op = op;
+  t.original = op;
   t.mapping = mapping;
-  t.plan = plan_for(op, intr, mapping, mr.bind);
-  // The reference schedule (split mapped loops by the instruction extents,
-  // outer pieces outside, pragma over the inner pieces), recorded as text.
-  // Members of a fused group must be adjacent before they are fused: if the
-  // op declares them apart (conv2d_tdsl's ko ... ki), reorder first.
+  ComputeOp cur = op;
+  // the fused group (outermost first) ending in each mapped op loop
+  auto group_of = [&](const std::string& o, const std::string& i) {
+    std::vector<std::string> g;
+    auto f = mapping.fused.find(i);
+    if (f != mapping.fused.end()) g = f->second;
+    g.push_back(o);
+    return g;
+  };
+  for (const auto& [o, i] : mapping.f) {
+    const LoopVar* il = intr.semantics.find_loop(i);
+    const LoopVar* ol = op.find_loop(o);
+    if (!il || !ol) throw ScheduleError("mapping names an unknown loop (" + o + " -> " + i + ")");
+    int64_t extent = 1;
+    for (const auto& g : group_of(o, i)) extent *= op.find_loop(g)->extent;
+    if (extent % il->extent == 0) continue;
+    if (!allow_pad)
+      throw DivisibilityError("loop '" + o + "' covers " + std::to_string(extent) + " iterations, not a multiple of " +
+                              intr.name + "'s '" + i + "' extent " + std::to_string(il->extent) +
+                              " (allow padding to proceed)");
+    if (device || group_of(o, i).size() > 1) continue;  // the device clips the tail
+    Transform pad;
+    pad.kind = Transform::Kind::Pad;
+    pad.a = o;
+    pad.factor = il->extent;
+    t.schedule.push_back(pad);
+    cur = pad_to_multiple(cur, o, il->extent);
+  }
+  // fused groups: members must be adjacent (declaration order), so reorder
+  // them together first when the op declares them apart (conv2d_tdsl's ko..ki)
+  std::map<std::string, std::string> axis_of;  // op loop -> the axis it becomes before the split
+  std::vector<std::string> order;
+  bool moved = false;
   {
-    std::vector<std::string> order, seen;
-    for (const auto& l : op.loops) {
-      if (in(seen, l.name)) continue;
-      std::vector<std::string> group{l.name};
+    std::set<std::string> placed;
+    for (const auto& l : cur.loops) {
+      if (placed.count(l.name)) continue;
+      std::vector<std::string> grp{l.name};
       for (const auto& [o, i] : mapping.f) {
-        auto f = mapping.fused.find(i);
-        if (f == mapping.fused.end() || f->second.empty()) continue;
-        std::vector<std::string> members = f->second;
-        members.push_back(o);
-        if (in(members, l.name)) group = members;
+        const auto g = group_of(o, i);
+        if (g.size() > 1 && std::count(g.begin(), g.end(), l.name)) grp = g;
       }
-      for (const auto& g : group) order.push_back(g), seen.push_back(g);
+      for (const auto& g : grp) {
+        moved = moved || order.size() >= cur.loops.size() || cur.loops[order.size()].name != g;
+        order.push_back(g);
+        placed.insert(g);
+      }
     }
-    bool moved = false;
-    for (size_t i = 0; i < order.size(); ++i) moved = moved || order[i] != op.loops[i].name;
-    if (moved) {
-      std::string ro = "reorder";
-      for (const auto& v : order) ro += " " + v;
-      t.schedule.push_back(ro);
-    }
+  }
+  if (moved) {
+    Transform ro;
+    ro.kind = Transform::Kind::Reorder;
+    ro.names = order;
+    t.schedule.push_back(ro);
   }
   for (const auto& [o, i] : mapping.f) {
-    const int64_t e = intr.semantics.find_loop(i)->extent;
-    std::string axis = o;
-    auto f = mapping.fused.find(i);
-    if (f != mapping.fused.end()) {
-      for (auto it = f->second.rbegin(); it != f->second.rend(); ++it) {
-        t.schedule.push_back("fuse " + *it + " " + axis);
-        axis = *it + "." + axis + ".fused";
-      }
+    const auto g = group_of(o, i);
+    std::string axis = g.back();
+    for (size_t k = g.size() - 1; k-- > 0;) {  // fuse outward: (oh, ow) -> oh.ow.fused, then (n, ...)
+      Transform fu;
+      fu.kind = Transform::Kind::Fuse;
+      fu.a = g[k];
+      fu.b = axis;
+      t.schedule.push_back(fu);
+      axis = g[k] + "." + axis + ".fused";
     }
-    t.schedule.push_back("split " + axis + " " + std::to_string(e));
+    for (const auto& x : g) axis_of[x] = axis;
+    Transform sp;
+    sp.kind = Transform::Kind::Split;
+    sp.a = axis;
+    sp.factor = intr.semantics.find_loop(i)->extent;
+    t.schedule.push_back(sp);
     t.pragma_axes.push_back(axis + ".i");
-    (op.find_loop(o)->kind == LoopKind::DataParallel ? t.outer_dp : t.outer_red).push_back(axis + ".o");
   }
-  for (const auto& l : op.loops)
-    if (mapping.instr_loop_of(l.name).empty()) (l.kind == LoopKind::DataParallel ? t.outer_dp : t.outer_red).push_back(l.name);
-  std::string ro = "reorder";
-  for (const auto& v : t.outer_dp) ro += " " + v;
-  for (const auto& v : t.outer_red) ro += " " + v;
-  for (const auto& v : t.pragma_axes) ro += " " + v;
+  {
+    std::set<std::string> done;
+    for (const auto& name : order) {
+      const LoopVar* l = cur.find_loop(name);
+      auto it = axis_of.find(name);
+      const std::string n = it == axis_of.end() ? name : it->second + ".o";
+      if (!done.insert(n).second) continue;  // a fused group's axis appears once
+      (l->kind == LoopKind::DataParallel ? t.outer_dp : t.outer_red).push_back(n);
+    }
+  }
+  Transform ro;
+  ro.kind = Transform::Kind::Reorder;
+  ro.names = t.outer_dp;
+  ro.names.insert(ro.names.end(), t.outer_red.begin(), t.outer_red.end());
+  ro.names.insert(ro.names.end(), t.pragma_axes.begin(), t.pragma_axes.end());
   t.schedule.push_back(ro);
-  std::string pg = "pragma";
-  for (const auto& v : t.pragma_axes) pg += " " + v;
+  Transform pg;
+  pg.kind = Transform::Kind::Pragma;
+  pg.names = t.pragma_axes;
   t.schedule.push_back(pg);
+  t.op = std::move(cur);
+  if (device) {
+    MatchResult mr = match_operation(op, intr);
+    if (!mr.ok) throw InjectError("no structural match: " + mr.reason);
+    t.plan = plan_for(op, intr, mapping, mr.bind);
+    t.has_plan = true;
+  }
   return t;
 }
 
 TensorizedOp tensorize(const ComputeOp& op, const Intrinsic& intr) {
   MatchResult mr = match_operation(op, intr);
   if (!mr.ok) throw InjectError("no structural match: " + mr.reason);
+  if (!is_tcgen05(intr))
+    throw NoFeasibleMapping("no mapping of '" + intr.name + "' has an sm_100a kernel (mnemonic '" +
+                            intr.target_mnemonic + "'; this backend executes tcgen05 descriptions)");
   std::string last;
   for (const auto& m : enumerate_group_mappings(op, intr, mr.bind)) {
     try {
@@ -568,6 +630,8 @@ Epi epilogue_of(const ComputeOp& main, const ComputeOp* ep) {
 void run_tensorized_packed(const TensorizedOp& t, const std::map<std::string, const void*>& host, void* host_out,
                            int64_t out_bytes, const ComputeOp* epilogue_op) {
   using namespace tzcb200;
+  if (!t.has_plan)
+    throw InjectError("no sm_100a kernel for this tensorized op (only tcgen05 descriptions execute on the B200)");
   const KernelPlan& p = t.plan;
   const ComputeOp& op = t.op;
   const Epi ep = epilogue_of(op, epilogue_op);

@@ -431,11 +431,10 @@ StmtPtr nest_over(const std::vector<std::string>& names, const std::vector<int64
 
 }  // namespace
 
-TensorIR lower(const ComputeOp& op, const Schedule& schedule, const LowerOptions& opts) {
-  if (!schedule.empty() && schedule.front().kind == Transform::Kind::Pad)
-    throw PadUnsupported("pad '" + schedule.front().a +
-                         "': this backend pads inside the kernel (TMA out-of-bounds zero fill); "
-                         "use tile_and_reorder's plan");
+namespace {
+
+// The nest of an (already padded) op under the axis transforms of a schedule.
+TensorIR lower_axes(const ComputeOp& op, const Schedule& schedule, const LowerOptions& opts) {
   Nest nest(op, opts.clip_tails);
   for (const auto& t : schedule) nest.apply(t);
   nest.check_pragma_innermost();
@@ -518,10 +517,15 @@ TensorIR lower(const ComputeOp& op, const Schedule& schedule, const LowerOptions
   return ir;
 }
 
-TensorIR lower(const ComputeOp& op, const std::vector<std::string>& lines, const LowerOptions& opts) {
-  std::string text;
-  for (const auto& l : lines) text += l + "\n";
-  return lower(op, parse_schedule(text), opts);
+}  // namespace
+
+TensorIR lower(const ComputeOp& op, const Schedule& schedule, const LowerOptions& opts) {
+  // leading pads reshape the op itself (zero extension); the rest are axis transforms
+  ComputeOp cur = op;
+  size_t i = 0;
+  for (; i < schedule.size() && schedule[i].kind == Transform::Kind::Pad; ++i)
+    cur = pad_to_multiple(cur, schedule[i].a, schedule[i].factor);
+  return lower_axes(cur, Schedule(schedule.begin() + (std::ptrdiff_t)i, schedule.end()), opts);
 }
 
 // ============================ inject =====================================

@@ -84,7 +84,7 @@ def test_cli_exit_codes(tmp_path):
     mm = os.path.join(ROOT, "tests", "golden", "tnsr", "mm_i8", "op.tdsl")
     shutil.copy(mm, tmp_path / "mm.tdsl")
     rc, _, err = cli("run", str(tmp_path / "mm.tdsl"), "--intrinsic", "vdot_16x4")
-    assert rc == 1 and "InjectError" in err
+    assert rc == 1 and ("InjectError" in err or "NoFeasibleMapping" in err) and "sm_100a kernel" in err
 
 
 @needs_cli
