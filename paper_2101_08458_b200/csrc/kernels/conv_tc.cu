@@ -24,6 +24,7 @@
 #include "conv_tc.cuh"
 #include "conv_tc2.cuh"
 #include "conv_ws.cuh"
+#include "stem_ws.cuh"
 
 #ifdef TZC_TRACE
 int g_debug_flags = 0;  // tools/trace_ws only
@@ -415,6 +416,7 @@ Problem s2d_problem(const Problem& pb);
 // runs, the space-to-depth rewrite for the stem)?  A forced split-K (the
 // op's split_reduction schedule or the "splits" option) runs on the general
 // kernel, which implements it; so does everything the ws kernel cannot hold.
+bool stem_fused_eligible(const Problem& pb, const Options& o);
 bool ws_route(const Problem& pb, const Options& o, Problem* q, WsPlan* w, bool* s2d) {
   const bool k7 = needs_k7(pb);
   const int forced = pb.forced_splits ? pb.forced_splits : o.splits;
@@ -443,7 +445,8 @@ Status plan_problem(const Problem& pb_in, const Options& o, tzc_plan* plan) {
       plan->smem_bytes = w.smem;
       plan->tiles_m = w.tiles;
       plan->tiles_n = 1;
-      plan->workspace_bytes = s2d ? (int64_t)q.n * q.hp * q.wp * 16 * (pb_in.f16 ? 2 : 1) : 0;
+      plan->workspace_bytes =
+          s2d && !stem_fused_eligible(pb_in, o) ? (int64_t)q.n * q.hp * q.wp * 16 * (pb_in.f16 ? 2 : 1) : 0;
       return Status();
     }
   }
@@ -732,6 +735,119 @@ Status run_ws(const Problem& pb, const WsPlan& w, const Options& o, const void* 
   return fn(p, w.grid, w.smem, stream);
 }
 
+// ---- the fused space-to-depth stem (stem_ws.cuh) ----------------------------
+// Eligible: int8 C = 3 stride-2 stems whose space-to-depth problem has a pair
+// plan (ws_plan), 16-byte aligned input, 32-bit byte offsets.  q = the S2D
+// problem (s2d_problem), w = its plan.
+bool stem_fused_eligible(const Problem& pb, const Options& o) {
+  return o.stem_fused && !pb.f16 && pb.c == 3 && pb.stride == 2 && pb.r <= 8 && pb.s <= 8 &&
+         (int64_t)pb.n * pb.hp * pb.wp * 3 < (int64_t(1) << 31) - 65536;
+}
+
+template <int BN, int EPM>
+Status launch_stem(const ConvKernelParams& p, int grid, int smem, cudaStream_t stream) {
+  auto kern = tzcdev::stem_ws_kernel<BN, EPM>;
+  static std::atomic<uint64_t> attr_done{0};
+  Status sa = ensure_smem_attr(kern, attr_done);
+  if (!sa.ok()) return sa;
+  cudaError_t e = launch_pdl(kern, dim3(grid), dim3(tzcdev::EpiCfg<BN>::THREADS), smem, stream, p);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  if (e == cudaSuccess) e = cudaGetLastError();
+  if (e != cudaSuccess) return Status(TZC_E_DEVICE, std::string("stem_ws launch: ") + cudaGetErrorString(e));
+  return Status();
+}
+
+Status run_stem_fused(const Problem& pb, const Problem& q, const WsPlan& w, const Options& o, const void* x,
+                      const void* wt, const void* seed, void* out, const tzc_epilogue& ep, cudaStream_t stream) {
+  ConvKernelParams p;
+  std::memset(&p, 0, sizeof(p));
+  // raw bytes one work unit needs: from its first S2D row's first raw byte to
+  // the last byte of its last pixel's two raw rows (exact, over all units)
+  const int64_t hw4 = (int64_t)q.hp * q.wp, P = (int64_t)q.n * hw4, unit = (int64_t)w.mt * 128;
+  int64_t need = 0;
+  for (int64_t q0 = 0; q0 < P; q0 += unit) {
+    const int64_t n0 = q0 / hw4, i0 = (q0 % hw4) / q.wp;
+    const int64_t base = ((n0 * pb.hp + 2 * i0) * pb.wp * 3) & ~int64_t(15);  // 16-byte aligned box start
+    const int64_t ql = std::min(q0 + w.sr, P) - 1;
+    const int64_t n = ql / hw4, i = (ql % hw4) / q.wp;
+    const int64_t h = std::min<int64_t>(2 * i + 1, pb.hp - 1);
+    const int64_t end = ((n * pb.hp + h) * pb.wp + pb.wp) * 3;  // through the end of that raw row
+    need = std::max(need, end - base);
+  }
+  p.raw_boxes = (int)((need + 255) / 256);
+  // + slack: the transform reads a masked row h+1 one raw row past the last
+  // staged byte (odd image heights), and 12-byte word groups past a row end
+  p.raw_slot = ((p.raw_boxes * 256 + pb.wp * 3 + 64 + 1023) / 1024) * 1024;
+  const int b_bytes = ((16 * w.bn * 16 + 1023) / 1024) * 1024;
+  const int a_slot = ((w.sr * 16 + 1023) / 1024) * 1024;
+  int a_slots = 4, r_slots = 3;
+  auto smem_of = [&](int as, int rs) { return 1024 + b_bytes + as * a_slot + rs * p.raw_slot + 512; };
+  while (smem_of(a_slots, r_slots) > 227 * 1024 - kStaticSmem && (a_slots > 2 || r_slots > 2)) {
+    if (a_slots >= r_slots && a_slots > 2) --a_slots;
+    else --r_slots;
+  }
+  const int smem = smem_of(a_slots, r_slots);
+  if (smem > 227 * 1024 - kStaticSmem) return Status(TZC_E_INTERNAL, "fused stem: shared memory");
+  {  // A: the input as a 1-D byte tensor (TMA boxes of 256 bytes, 16-byte aligned starts)
+    cuuint64_t dims[1] = {(cuuint64_t)pb.n * pb.hp * pb.wp * 3};
+    cuuint64_t strides[1] = {dims[0]};  // rank 1 has no strides; the driver wants a valid array
+    cuuint32_t box[1] = {256};
+    cuuint32_t es[1] = {1};
+    Status st = enc_check(p_encode_tiled(&p.tmA, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, const_cast<void*>(x), dims, strides,
+                                         box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE),
+                          "cuTensorMapEncodeTiled(stem raw)");
+    if (!st.ok()) return st;
+  }
+  p.wraw = wt;
+  if (const char* dbg = std::getenv("TZC_STEM_DEBUG")) p.debug_flags = std::atoi(dbg);  // bring-up only
+  p.w_sk = pb.w_stride_k;
+  p.w_st = pb.w_stride_tap;
+  p.w_r = pb.r;
+  p.w_s = pb.s;
+  p.raw_hp = pb.hp;
+  p.raw_wp = pb.wp;
+  p.raw_c = 3;
+  p.raw_slots = r_slots;
+  p.M = (int32_t)pb.m;
+  p.Ngemm = pb.ngemm;
+  p.Hp = q.hp;
+  p.Wp = q.wp;
+  p.OH = pb.oh;
+  p.OWv = pb.ow;
+  p.P = (int32_t)P;
+  p.SR = w.sr;
+  {  // MMA table: pair MMAs over taps (r, s), (r, s+1) of the 4 x 4 S2D filter
+    int i = 0;
+    for (int r = 0; r < 4; ++r)
+      for (int s = 0; s < 4; s += 2, ++i) {
+        p.mma_a[i] = (uint32_t)(r * q.wp + s);
+        p.mma_b[i] = (uint32_t)(((r * 4 + s) * w.bn * 16) >> 4);
+      }
+    p.n_mma = i;
+  }
+  p.magic_hw = ((uint64_t(1) << 40) + (uint64_t)hw4 - 1) / (uint64_t)hw4;
+  p.magic_wp = ((uint64_t(1) << 40) + (uint64_t)q.wp - 1) / (uint64_t)q.wp;
+  p.magic_wp32 = (uint32_t)(((uint64_t(1) << 32) + (uint64_t)q.wp - 1) / (uint64_t)q.wp);
+  if ((int64_t)w.sr + q.wp >= 65536) return Status(TZC_E_INTERNAL, "fused stem: unit too long for the 16-bit divide");
+  p.num_tiles = w.tiles;
+  p.splits = a_slots;
+  p.mt = w.mt;
+  p.nacc = o.ws_epi_groups == 2 ? 2 : std::min(4, 512 / (w.mt * w.bn));
+  p.epi_groups = o.ws_epi_groups == 2 ? 2 : 1;
+  fill_epilogue(&p, pb, o, seed, out, ep);
+  const bool rq = ep.kind == tzcdev::EP_REQUANT_I8;
+  if (ep.kind != tzcdev::EP_I32 && !rq) return Status(TZC_E_TYPE, "fused stem: int8 ops take i32 or requant epilogues");
+  switch (w.bn) {
+    case 64: return rq ? launch_stem<64, tzcdev::EPM_REQUANT>(p, w.grid, smem, stream)
+                       : launch_stem<64, tzcdev::EPM_RAW>(p, w.grid, smem, stream);
+    case 128: return rq ? launch_stem<128, tzcdev::EPM_REQUANT>(p, w.grid, smem, stream)
+                        : launch_stem<128, tzcdev::EPM_RAW>(p, w.grid, smem, stream);
+    default: return rq ? launch_stem<256, tzcdev::EPM_REQUANT>(p, w.grid, smem, stream)
+                       : launch_stem<256, tzcdev::EPM_RAW>(p, w.grid, smem, stream);
+  }
+}
+
 // Space-to-depth geometry for a stride-2 conv with 4*C*e <= 16 (the stem).
 // int8: 16-byte S2D pixels (pair mode); fp16: C = 3 only (12 of 16 halfs per
 // 32-byte pixel, one K=16 MMA per tap), even padded extents.
@@ -814,6 +930,7 @@ Status run_problem(const Problem& pb, const Options& o, const void* a, const voi
     WsPlan w;
     if (ws_route(pb, o, &q, &w, &s2d)) {
       if (!s2d) return run_ws(pb, w, o, a, b, seed, out, ep, stream);
+      if (stem_fused_eligible(pb, o)) return run_stem_fused(pb, q, w, o, a, b, seed, out, ep, stream);
       // the stem: space-to-depth to 16-byte pixels, then the shifted-window
       // kernel in pair mode (two taps per K=32 MMA)
       void* x4 = nullptr;

@@ -146,6 +146,16 @@ struct alignas(64) ConvKernelParams {
   uint32_t mma_a[64], mma_b[64];
   // divisors of the general kernel's per-tile index math
   FastDiv fd_splits, fd_tiles_n, fd_ohow, fd_ow, fd_cblocks, fd_s;
+  // fused space-to-depth stem (stem_ws.cuh): raw NHWC input geometry, raw
+  // staging per work unit (tmA is then a 1-D byte map of the input), raw
+  // [K,R,S,C] weights rearranged in the prologue
+  const void* wraw;
+  int64_t w_sk, w_st;          // raw weight strides (elements): k, tap
+  int32_t raw_hp, raw_wp, raw_c, w_r, w_s;
+  int32_t raw_boxes;           // 256-byte TMA boxes per unit's raw staging
+  int32_t raw_slot;            // bytes per raw staging slot
+  int32_t raw_slots;           // raw staging ring depth
+  uint32_t magic_wp32;         // ceil(2^32 / Wp4): t / Wp4 = umulhi(t, magic) for t < 2^16
 };
 
 template <int BN, int KB>

@@ -64,6 +64,19 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+// Spin variant: mbarrier.test_wait (never suspends the thread) — for handoffs
+// on the critical path where a suspended warp's wake-up latency would show.
+__device__ __forceinline__ void mbar_wait_spin(uint64_t* bar, uint32_t parity) {
+  uint32_t addr = smem_u32(bar);
+  asm volatile(
+      "{\n\t.reg .pred P;\n"
+      "SPIN_%=:\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 P, [%0], %1;\n\t"
+      "@!P bra SPIN_%=;\n\t}" ::"r"(addr),
+      "r"(parity)
+      : "memory");
+}
+
 // ---- TMA -------------------------------------------------------------------
 __device__ __forceinline__ void tma_prefetch(const void* tmap) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(tmap)) : "memory");
@@ -102,6 +115,15 @@ __device__ __forceinline__ void tma_load_3d_hint(void* dst, const void* tmap, ui
       "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
       " [%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(smem_u32(dst)),
       "l"(reinterpret_cast<uint64_t>(tmap)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "l"(pol)
+      : "memory");
+}
+// 1-D tiled box (byte tensors) at element offset c0; the box start must be
+// 16-byte aligned (an unaligned start faults: tools/tma1d_test).
+__device__ __forceinline__ void tma_load_1d_hint(void* dst, const void* tmap, uint64_t* bar, int c0, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.1d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%3}], [%2], %4;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(smem_u32(bar)), "r"(c0), "l"(pol)
       : "memory");
 }
 __device__ __forceinline__ void tma_load_2d_p(void* dst, const void* tmap, uint64_t* bar, int c0, int c1,

@@ -95,7 +95,7 @@ FORCED = [
     ("c2_3x3_64", 5, 58, 64, 64, 3, 1),
     ("c2_1x1_64_64", 7, 56, 64, 64, 1, 1),
     ("3x3_64_128", 4, 30, 64, 128, 3, 1),   # BN = 128: MT <= 2 (2 * MT * BN <= 512 TMEM columns)
-    ("3x3_128_64_small", 11, 16, 128, 64, 3, 1),  # Wp < 32: a lane quarter's 32 rows span image rows
+    ("3x3_64_64_small", 11, 16, 64, 64, 3, 1),  # Wp < 32: a lane quarter's 32 rows span image rows
 ]
 
 

@@ -45,19 +45,26 @@ def test_ws_conv_bitexact(cuda, n, hp, c, k, r):
     assert np.array_equal(q, Orc.requant_i8(Orc.conv2d_nhwc(x, w, 1), scale))
 
 
-@pytest.mark.parametrize("n,hp,k", [(2, 230, 64), (1, 62, 64), (3, 62, 128), (2, 61, 64)])
-def test_s2d_stem_bitexact(cuda, n, hp, k):
-    """7x7 stride-2 over C=3: space-to-depth to 16-byte pixels + the pair-mode kernel."""
+@pytest.mark.parametrize("fused", [0, 1])
+@pytest.mark.parametrize("n,hp,k", [(2, 230, 64), (1, 62, 64), (3, 62, 128), (2, 61, 64), (5, 230, 256)])
+def test_s2d_stem_bitexact(cuda, n, hp, k, fused):
+    """7x7 stride-2 over C=3: space-to-depth to 16-byte pixels + the pair-mode
+    kernel; fused=1: the space-to-depth done inside the kernel (stem_ws.cuh:
+    raw 1-D TMA staging -> transform warps), incl. odd extents (61)."""
     x = Orc.random_tensor("u8", (n, hp, hp, 3), 310)
     w = Orc.random_tensor("i8", (k, 7, 7, 3), 311)
     ref = Orc.conv2d_nhwc(x, w, 2)
-    assert np.array_equal(run(cuda, x, w, 2), ref)
-    o = (hp - 7) // 2 + 1
-    s0 = Orc.random_tensor("i32", (n, o, o, k), 312)
-    assert np.array_equal(run(cuda, x, w, 2, s0), Orc.conv2d_nhwc(x, w, 2, s0))
-    scale = 2.0 ** -11
-    q = run(cuda, x, w, 2, None, epilogue="requant_i8", scale=scale)
-    assert np.array_equal(q, Orc.requant_i8(ref, scale))
+    D.set_option("stem_fused", fused)
+    try:
+        assert np.array_equal(run(cuda, x, w, 2), ref)
+        o = (hp - 7) // 2 + 1
+        s0 = Orc.random_tensor("i32", (n, o, o, k), 312)
+        assert np.array_equal(run(cuda, x, w, 2, s0), Orc.conv2d_nhwc(x, w, 2, s0))
+        scale = 2.0 ** -11
+        q = run(cuda, x, w, 2, None, epilogue="requant_i8", scale=scale)
+        assert np.array_equal(q, Orc.requant_i8(ref, scale))
+    finally:
+        D.set_option("stem_fused", 0)
 
 
 def test_ws_blocked_output_layout(cuda):

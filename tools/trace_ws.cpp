@@ -72,7 +72,7 @@ int main(int argc, char** argv) {
              (long long)(t[11 + 5 * i] - t[0]), (long long)(t[12 + 5 * i] - t[0]), (long long)(t[70 + i] - t[0]), (long long)(t[13 + 5 * i] - t[0]),
              (long long)(t[14 + 5 * i] - t[0]));
     for (int i = 0; i < 10; ++i)
-      printf("  tile %d: mmaLoopTop=%lld temptyOk=%lld lastEpiWarpEnd=%lld epiLoopTop=%lld\n", i, (long long)(t[80 + i] - t[0]),
+      printf("  tile %d: mmaLoopTop=%lld temptyOk=%lld xformStart=%lld xformEnd=%lld\n", i, (long long)(t[80 + i] - t[0]),
              (long long)(t[90 + i] - t[0]), (long long)(t[100 + i] - t[0]), (long long)(t[110 + i] - t[0]));
   }
   {
