@@ -34,7 +34,8 @@ const Knob kKnobs[] = {
     {"shifted_window", &Options::shifted_window, 0, 1, nullptr},
     {"ws_epi_groups", &Options::ws_epi_groups, 1, 2, kEgAllowed},
     {"tail_split", &Options::tail_split, 0, 1, nullptr},
-    {"split_min_kb", &Options::split_min_kb, 1, 1 << 20, nullptr},
+    {"split_min_kb", &Options::split_min_kb, 0, 1 << 20, nullptr},
+    {"splitk_inkernel", &Options::splitk_inkernel, 0, 1, nullptr},
     {"pingpong_kb", &Options::pingpong_kb, 0, 1 << 20, nullptr},
     {"ws_mt", &Options::ws_mt, 0, 4, kMtAllowed},
     {"ws_1x1_k", &Options::ws_1x1_k, 0, 1 << 20, nullptr},

@@ -67,9 +67,13 @@ WorkSplit work_split(int tiles, int tiles_n, int num_kb, int sms, bool ok16, int
   }
   if (!ok16) return w;
   if (tiles < sms) {
-    // fill the machine, keeping >= 8 K blocks per split so the int32 partial
-    // round trip stays small next to the MMA work
-    const int s = std::min((sms + tiles - 1) / tiles, num_kb / std::max(1, o.split_min_kb));
+    // fill the machine, keeping >= split_min_kb K blocks per split (0: off).
+    // Off by default: measured at batch 32 (profiles/r02_summary.md §6) a
+    // split costs more than the idle SMs it fills even with the in-kernel
+    // fix-up (c5_3x3_512: 15.4 us unsplit, 17.5-34 us split 2-4 ways), and in
+    // the multi-branch step other layers' CTAs fill those SMs anyway.
+    const int min_kb = o.split_min_kb > 0 ? o.split_min_kb : (1 << 20);
+    const int s = std::min(std::min((sms + tiles - 1) / tiles, 4), num_kb / std::max(1, min_kb));
     if (s >= 2) {
       w.splits = s;
       w.full = 0;
@@ -281,6 +285,11 @@ Status launch_impl(const ConvKernelParams& p, int grid, cudaStream_t stream) {
                   : (p.ep_kind == tzcdev::EP_CAST_F16) ? tzcdev::EPM_F16
                                                        : tzcdev::EPM_RAW;
   constexpr int kAlt = F16 ? tzcdev::EPM_F16 : tzcdev::EPM_REQUANT;
+  if (p.splits > 1 && p.splitk_cnt) {  // split-K with the in-kernel fix-up: one launch, the real epilogue
+    if (epm == tzcdev::EPM_RAW) return launch_kernel<BN, KB, F16, AM, BMN, tzcdev::EPM_RAW>(p, grid, stream);
+    if ((epm == tzcdev::EPM_F16) != F16) return Status(TZC_E_TYPE, "epilogue kind does not match the profile");
+    return launch_kernel<BN, KB, F16, AM, BMN, kAlt>(p, grid, stream);
+  }
   if (p.splits > 1 && p.full_units == 0) {  // classic split-K: every unit writes partials
     ConvKernelParams pk = p;
     pk.ep_kind = tzcdev::EP_PARTIAL;  // raw partials; the fix-up applies the epilogue
@@ -345,9 +354,9 @@ Status enc_check(CUresult r, const char* what) {
 // would make that graph's next replay read freed memory.  Growth is
 // geometric, so the retired bytes stay below the live ones.
 std::mutex g_ws_mu;
-struct Scratch {
-  void* p[3] = {nullptr, nullptr, nullptr};
-  size_t bytes[3] = {0, 0, 0};
+struct Scratch {  // slot 3: split-K arrival counters (zeroed when allocated)
+  void* p[4] = {nullptr, nullptr, nullptr, nullptr};
+  size_t bytes[4] = {0, 0, 0, 0};
 };
 std::map<std::pair<int, cudaStream_t>, Scratch> g_ws;
 std::vector<void*> g_ws_retired;
@@ -365,6 +374,10 @@ Status workspace(int slot, size_t bytes, void** out, cudaStream_t stream) {
     void* p = nullptr;
     cudaError_t e = cudaMalloc(&p, want);
     if (e != cudaSuccess) return Status(TZC_E_DEVICE, std::string("workspace: ") + cudaGetErrorString(e));
+    if (slot == 3) {  // counters start at zero; every use leaves them zero again
+      e = cudaMemset(p, 0, want);
+      if (e != cudaSuccess) return Status(TZC_E_DEVICE, std::string("workspace: ") + cudaGetErrorString(e));
+    }
     if (s.p[slot]) g_ws_retired.push_back(s.p[slot]);
     s.p[slot] = p;
     s.bytes[slot] = want;
@@ -1097,6 +1110,12 @@ Status run_problem(const Problem& pb, const Options& o, const void* a, const voi
   if (plan.splits > 1) {
     st = workspace(0, (size_t)plan.workspace_bytes, &p.partial, stream);
     if (!st.ok()) return st;
+    if (o.splitk_inkernel) {
+      void* cnt = nullptr;
+      st = workspace(3, (size_t)p.num_tiles * 16 * sizeof(int32_t), &cnt, stream);
+      if (!st.ok()) return st;
+      p.splitk_cnt = static_cast<int32_t*>(cnt);
+    }
   }
   const Entry* ent = find_entry(plan.bn, plan.bk_bytes, pb.f16, pb.a_mode, pb.b_kn);
   return ent->fn(p, plan.grid, stream);

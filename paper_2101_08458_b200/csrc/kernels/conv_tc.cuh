@@ -156,6 +156,10 @@ struct alignas(64) ConvKernelParams {
   int32_t raw_slot;            // bytes per raw staging slot
   int32_t raw_slots;           // raw staging ring depth
   uint32_t magic_wp32;         // ceil(2^32 / Wp4): t / Wp4 = umulhi(t, magic) for t < 2^16
+  // split-K fixed up inside the kernel: per (tile, epilogue-warp slice)
+  // arrival counters (16 per tile, zero between launches); null = the
+  // separate fix-up kernel (splitk_reduce_kernel)
+  int32_t* splitk_cnt;
 };
 
 template <int BN, int KB>
@@ -680,6 +684,7 @@ __global__ void __launch_bounds__(EpiCfg<BN>::THREADS, 1) conv_tc_kernel(const _
       // otherwise (ragged channels, odd strides) the element-wise one
       const bool fast = p.vec_ok && (n_tile + 1) * BN <= p.Ngemm;
       const uint32_t tq = tmem_base + ((q * 32) << 16) + acc * BN;
+      bool released = false;
       if (p.debug_flags & 1) {
       } else if (split >= 0) {  // K-split unit: raw partial sums for the fix-up kernel
 #pragma unroll 1
@@ -694,6 +699,71 @@ __global__ void __launch_bounds__(EpiCfg<BN>::THREADS, 1) conv_tc_kernel(const _
 #pragma unroll
             for (int j = 0; j < CW / 4; ++j)
               if (n + 4 * j < p.Ngemm) st_v4(o + 4 * j, v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+          }
+        }
+        if (p.splitk_cnt) {
+          // In-kernel fix-up (no second launch): every split stores its raw
+          // partial slice; the LAST split to finish this warp's slice of the
+          // tile (a per-slice arrival counter) adds all splits' partials and
+          // runs the real epilogue.  Release/acquire: each writer fences its
+          // stores before the counter increment, the last arriver fences after
+          // observing the final count.  Integer partials wrap-add (associative:
+          // bit-identical to any order, F8); fp32 partials are added in split
+          // order.  The counter is reset by the last arriver for the next launch.
+          tc_fence_before();  // TMEM reads of this unit are complete: hand the buffer back early
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty[acc]);
+          released = true;
+          const int slot = (int)((warp - 4) % (16 / EG));
+          int32_t* cnt = p.splitk_cnt + (int64_t)tile * 16 + slot;
+          asm volatile("fence.acq_rel.gpu;" ::: "memory");  // release this lane's partial stores
+          __syncwarp();
+          int prev = 0;
+          if (lane == 0) prev = atomicAdd(cnt, 1);
+          prev = __shfl_sync(0xffffffffu, prev, 0);
+          if (prev == p.splits - 1) {
+            asm volatile("fence.acq_rel.gpu;" ::: "memory");  // acquire the other splits' partials
+            if (lane == 0) *cnt = 0;
+#pragma unroll 1
+            for (int c = 0; c < HALF / CW; ++c) {
+              const int col = h * HALF + c * CW;
+              const int n = n_tile * BN + col;
+              uint32_t v[CW];
+#pragma unroll
+              for (int i = 0; i < CW; ++i) v[i] = 0u;
+              if (m < p.M) {
+#pragma unroll 1
+                for (int sp = 0; sp < p.splits; ++sp) {
+                  const uint32_t* src = static_cast<const uint32_t*>(p.partial) +
+                                        ((int64_t)sp * p.red_rows + (m - p.red_m0)) * p.Ngemm + n;
+                  // all of this split's loads in flight before the adds (.cg:
+                  // L2, never a stale L1 line); full-width pieces only
+                  uint4 tv[CW / 4];
+#pragma unroll
+                  for (int j = 0; j < CW / 4; ++j)
+                    tv[j] = n + 4 * j < p.Ngemm ? __ldcg(reinterpret_cast<const uint4*>(src + 4 * j))
+                                                : make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+                  for (int j = 0; j < CW / 4; ++j) {
+                    {
+                      const uint4 t = tv[j];
+                      if constexpr (kF16) {
+                        v[4 * j + 0] = __float_as_uint(__uint_as_float(v[4 * j + 0]) + __uint_as_float(t.x));
+                        v[4 * j + 1] = __float_as_uint(__uint_as_float(v[4 * j + 1]) + __uint_as_float(t.y));
+                        v[4 * j + 2] = __float_as_uint(__uint_as_float(v[4 * j + 2]) + __uint_as_float(t.z));
+                        v[4 * j + 3] = __float_as_uint(__uint_as_float(v[4 * j + 3]) + __uint_as_float(t.w));
+                      } else {
+                        v[4 * j + 0] += t.x;
+                        v[4 * j + 1] += t.y;
+                        v[4 * j + 2] += t.z;
+                        v[4 * j + 3] += t.w;
+                      }
+                    }
+                  }
+                }
+              }
+              epi_regs<CW, kF16, kEpm, BN>(p, v, (m < p.M && !(p.debug_flags & 2)) ? m : -1, n, fast);
+            }
           }
         }
       } else if (kEpm == EPM_REQUANT && p.tma_store) {
@@ -731,11 +801,13 @@ __global__ void __launch_bounds__(EpiCfg<BN>::THREADS, 1) conv_tc_kernel(const _
                                         fast);
         }
       }
-      tc_fence_before();
-      __syncwarp();
+      if (!released) {
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[acc]);
+      }
       if (threadIdx.x == 128 && it < 10) TZC_TRACE_POINT(14 + 5 * it);
       if (threadIdx.x == 128 + 256 && it < 10) TZC_TRACE_POINT(14 + 5 * it);
-      if (lane == 0) mbar_arrive(&tempty[acc]);
       if (EG == 2) {
         acc_phase ^= 1;
       } else if (++acc == 2) {

@@ -50,7 +50,8 @@ struct Options {
   int shifted_window = 1;       // weight-stationary kernel for eligible stride-1 convs
   int ws_epi_groups = 1;        // shifted window: 1 or 2 (ping-pong) epilogue groups
   int tail_split = 0;           // split the under-filled last round of tiles along K
-  int split_min_kb = 1 << 20;   // automatic split-K keeps >= this many K blocks per split (off)
+  int split_min_kb = 0;         // automatic split-K keeps >= this many K blocks per split (0: off)
+  int splitk_inkernel = 1;      // split-K partials combined inside the kernel (last-arriver fix-up)
   int pingpong_kb = 2;          // general kernel: ping-pong epilogue groups up to this many K blocks
   int ws_mt = 0;                // shifted window: force 1/2/4 tiles per work unit (0 = automatic)
   int ws_1x1_k = 64;            // shifted window for 1x1 convs with K <= this many bytes

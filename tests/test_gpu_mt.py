@@ -130,21 +130,25 @@ def test_forced_mt(cuda, name, nb, hp, c, k, r, st, mt, eg):
     assert np.array_equal(qg, Orc.requant_i8(ref, 0.000731))
 
 
-def test_forced_split_on_ws_layer_runs_split_k(cuda):
+@pytest.mark.parametrize("inkernel", [1, 0])
+def test_forced_split_on_ws_layer_runs_split_k(cuda, inkernel):
     """A forced split-K on a stride-1 3x3 conv (eligible for the shifted
-    window) must plan AND run on the general kernel with the fix-up launch
-    (the ws branch used to ignore it and report a plan it did not run)."""
+    window) must plan AND run on the general kernel as split-K (the
+    ws branch used to ignore it and report a plan it did not run): one launch
+    with the in-kernel fix-up, two with the separate fix-up kernel."""
     n, hp, c, k, r = 2, 16, 256, 128, 3
     x = Orc.random_tensor("u8", (n, hp, hp, c), 530)
     w = Orc.random_tensor("i8", (k, r, r, c), 531)
     D.set_splits(3)
+    D.set_option("splitk_inkernel", inkernel)
     try:
         d, _ = D.conv_desc(x.shape, w.shape, 1)
         plan = D.plan_conv(d)
         assert plan["splits"] == 3 and plan["a_mode"] == 1, plan
         c0 = D.launch_count()
         got = D.conv2d(to_dev(x, cuda), to_dev(w, cuda), 1).cpu().numpy()
-        assert D.launch_count() - c0 == 2  # conv_tc partials + splitk_reduce fix-up
+        assert D.launch_count() - c0 == (1 if inkernel else 2)
     finally:
         D.set_splits(0)
+        D.set_option("splitk_inkernel", 1)
     assert np.array_equal(got, Orc.conv2d_nhwc(x, w, 1))

@@ -198,11 +198,20 @@ def test_eval_tir_split_reduction_becomes_device_split_k(cuda):
     plain = "split x 128\nsplit y 128\nsplit k 32\nreorder x.o y.o k.o x.i y.i k.i\npragma x.i y.i k.i\n"
     split = ("split x 128\nsplit y 128\nsplit k 32\nsplit_reduction k.o 4\n"
              "reorder x.o y.o k.o.s k.o.r x.i y.i k.i\npragma x.i y.i k.i\n")
-    n0 = D.launch_count()
-    assert np.array_equal(ops.eval_tir(text, "tcgen05_i8_m128n128k32", ins, schedule=plain), ref)
-    n1 = D.launch_count()
+    # the in-kernel fix-up (default): one launch per op, bit-exact
     assert np.array_equal(ops.eval_tir(text, "tcgen05_i8_m128n128k32", ins, schedule=split), ref)
-    n2 = D.launch_count()
+    # with the separate fix-up kernel (and no automatic split) the fold launch is visible
+    D.set_option("splitk_inkernel", 0)
+    D.set_option("split_min_kb", 1 << 20)
+    try:
+        n0 = D.launch_count()
+        assert np.array_equal(ops.eval_tir(text, "tcgen05_i8_m128n128k32", ins, schedule=plain), ref)
+        n1 = D.launch_count()
+        assert np.array_equal(ops.eval_tir(text, "tcgen05_i8_m128n128k32", ins, schedule=split), ref)
+        n2 = D.launch_count()
+    finally:
+        D.set_option("splitk_inkernel", 1)
+        D.set_option("split_min_kb", 0)
     assert n2 - n1 > n1 - n0  # the fix-up (fold) kernel launched
     assert "C.partial" in ops.lower(text, split, "tcgen05_i8_m128n128k32")
 
