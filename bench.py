@@ -67,6 +67,8 @@ def parse():
     ap.add_argument("--branch-search", type=int, default=1,
                     help="1: choose the layer-to-branch assignment by measured step time before timing")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-flush", action="store_true",
+                    help="diagnostic only (never a reported number): skip the L2 flush between steps")
     ap.add_argument("--e2e-threads", type=int, default=3, help="host threads issuing run_op calls in the e2e leg")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="CPU baseline work budget")
@@ -448,7 +450,8 @@ def run_ours(args, rank, world, local):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 
     def step():
-        flush.zero_()                      # untimed: evict L2 between steps
+        if not args.no_flush:
+            flush.zero_()                  # untimed: evict L2 between steps
         torch.cuda.synchronize()
         with torch.cuda.stream(stream):   # replay() launches on the current stream
             e0.record(stream)

@@ -11,6 +11,10 @@ import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libtzc_b200.so")
+# TZC_B200_CHECKS=1 loads the instrumented build (libtzc_b200_checks.so:
+# mbarrier watchdogs and output-bounds asserts that trap; `make checks`)
+if os.environ.get("TZC_B200_CHECKS") == "1":
+    LIB_PATH = os.path.join(_HERE, "libtzc_b200_checks.so")
 
 TZC_OK = 0
 PROFILE_U8I8, PROFILE_F16 = 0, 1

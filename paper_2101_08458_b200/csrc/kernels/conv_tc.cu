@@ -198,9 +198,22 @@ namespace {
 // prologue (barrier init, TMEM alloc, descriptor prefetch) overlaps the
 // previous grid's tail; griddepcontrol.wait in the kernel keeps the data
 // dependency.  Captured into CUDA graphs as programmatic edges.
+#ifdef TZC_CHECKS
+// Instrumented build: the launch's legal store ranges (single-stream validation runs only).
+void set_check_bounds(const ConvKernelParams& p, cudaStream_t stream) {
+  unsigned long long lo[2] = {reinterpret_cast<unsigned long long>(p.out), reinterpret_cast<unsigned long long>(p.partial)};
+  unsigned long long hi[2] = {lo[0] + (unsigned long long)p.out_bytes, lo[1] + (unsigned long long)p.partial_bytes};
+  cudaMemcpyToSymbolAsync(tzcdev::g_chk_lo, lo, sizeof(lo), 0, cudaMemcpyHostToDevice, stream);
+  cudaMemcpyToSymbolAsync(tzcdev::g_chk_hi, hi, sizeof(hi), 0, cudaMemcpyHostToDevice, stream);
+}
+#endif
+
 template <typename Kern>
 cudaError_t launch_pdl(Kern kern, dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
                        const ConvKernelParams& p) {
+#ifdef TZC_CHECKS
+  set_check_bounds(p, stream);
+#endif
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = block;
@@ -252,6 +265,9 @@ Status launch_pair(const ConvKernelParams& p, int grid, cudaStream_t stream) {
   attr[1].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 2;
+#ifdef TZC_CHECKS
+  set_check_bounds(p, stream);
+#endif
   cudaError_t e = cudaLaunchKernelEx(&cfg, kern, p);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   if (e == cudaSuccess) e = cudaGetLastError();
@@ -892,6 +908,11 @@ void fill_epilogue(ConvKernelParams* pp, const Problem& pb, const Options& o, co
   ConvKernelParams& p = *pp;
   p.out = out;
   p.seed = seed;
+  {  // byte extent of the output layout (last element + 1)
+    const int eo = (ep.kind == tzcdev::EP_REQUANT_I8) ? 1 : (ep.kind == tzcdev::EP_CAST_F16) ? 2 : 4;
+    const int64_t nl = pb.ngemm - 1, nb = std::max<int64_t>(1, pb.out.nb);
+    p.out_bytes = ((nl / nb) * pb.out.stride_blk + (pb.m - 1) * pb.out.stride_m + nl % nb + 1) * eo;
+  }
   p.out_nb = pb.out.nb;
   p.out_stride_m = pb.out.stride_m;
   p.out_stride_blk = pb.out.stride_blk;
@@ -1108,6 +1129,7 @@ Status run_problem(const Problem& pb, const Options& o, const void* a, const voi
     return launch_pair_any(p, plan.bn, pb.a_mode, grid, stream);
   }
   if (plan.splits > 1) {
+    p.partial_bytes = plan.workspace_bytes;
     st = workspace(0, (size_t)plan.workspace_bytes, &p.partial, stream);
     if (!st.ok()) return st;
     if (o.splitk_inkernel) {

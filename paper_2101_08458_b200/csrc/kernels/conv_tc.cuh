@@ -160,6 +160,7 @@ struct alignas(64) ConvKernelParams {
   // arrival counters (16 per tile, zero between launches); null = the
   // separate fix-up kernel (splitk_reduce_kernel)
   int32_t* splitk_cnt;
+  int64_t out_bytes, partial_bytes;  // extents of out / partial (TZC_CHECKS bounds asserts)
 };
 
 template <int BN, int KB>
@@ -212,11 +213,34 @@ __device__ __forceinline__ uint32_t requant_general(int32_t c, float s) {
 }
 
 
+#ifdef TZC_CHECKS
+// Instrumented build: every epilogue store lies inside [out, out + out_bytes)
+// or [partial, partial + partial_bytes) (host-computed extents).
+__device__ unsigned long long g_chk_lo[2], g_chk_hi[2];
+__device__ __forceinline__ void chk_store(const void* ptr, int bytes) {
+  const unsigned long long a = reinterpret_cast<unsigned long long>(ptr);
+  bool ok = false;
+  for (int r = 0; r < 2; ++r) ok = ok || (a >= g_chk_lo[r] && a + bytes <= g_chk_hi[r]);
+  if (!ok) {
+    printf("tzc bounds: block %d thread %d stores %d bytes at %p outside the output / workspace\n", blockIdx.x,
+           threadIdx.x, bytes, ptr);
+    __trap();
+  }
+}
+#define TZC_CHK_STORE(p, n) chk_store((p), (n))
+#else
+#define TZC_CHK_STORE(p, n) \
+  do {                      \
+  } while (0)
+#endif
+
 __device__ __forceinline__ void st_v4(void* p, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  TZC_CHK_STORE(p, 16);
   asm volatile("st.global.v4.b32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(a), "r"(b), "r"(c), "r"(d)
                : "memory");
 }
 __device__ __forceinline__ void st_v8(void* p, const uint32_t* w) {  // 32-byte aligned
+  TZC_CHK_STORE(p, 32);
   asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p), "r"(w[0]), "r"(w[1]), "r"(w[2]),
                "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7])
                : "memory");
@@ -342,7 +366,10 @@ __device__ __forceinline__ void store16(const ConvKernelParams& p, int m, int n,
     } else {
 #pragma unroll
       for (int i = 0; i < 16; ++i)
-        if (n + i < p.Ngemm) static_cast<uint8_t*>(p.out)[out_offset(p, m, n + i)] = (uint8_t)(b[i] & 0xffu);
+        if (n + i < p.Ngemm) {
+          TZC_CHK_STORE(static_cast<uint8_t*>(p.out) + out_offset(p, m, n + i), 1);
+          static_cast<uint8_t*>(p.out)[out_offset(p, m, n + i)] = (uint8_t)(b[i] & 0xffu);
+        }
     }
   } else if constexpr (kEpm == EPM_F16) {
     uint32_t w[8];
@@ -362,7 +389,10 @@ __device__ __forceinline__ void store16(const ConvKernelParams& p, int m, int n,
     } else {
 #pragma unroll
       for (int i = 0; i < 16; ++i)
-        if (n + i < p.Ngemm) static_cast<uint16_t*>(p.out)[out_offset(p, m, n + i)] = (uint16_t)(w[i >> 1] >> (16 * (i & 1)));
+        if (n + i < p.Ngemm) {
+          TZC_CHK_STORE(static_cast<uint16_t*>(p.out) + out_offset(p, m, n + i), 2);
+          static_cast<uint16_t*>(p.out)[out_offset(p, m, n + i)] = (uint16_t)(w[i >> 1] >> (16 * (i & 1)));
+        }
     }
   } else {  // raw 32-bit accumulator image (i32 / f32)
     if constexpr (vec) {
@@ -377,7 +407,10 @@ __device__ __forceinline__ void store16(const ConvKernelParams& p, int m, int n,
     } else {
 #pragma unroll
       for (int i = 0; i < 16; ++i)
-        if (n + i < p.Ngemm) static_cast<uint32_t*>(p.out)[out_offset(p, m, n + i)] = a[i];
+        if (n + i < p.Ngemm) {
+          TZC_CHK_STORE(static_cast<uint32_t*>(p.out) + out_offset(p, m, n + i), 4);
+          static_cast<uint32_t*>(p.out)[out_offset(p, m, n + i)] = a[i];
+        }
     }
   }
 }

@@ -39,7 +39,8 @@ def conv(n, hp, c, k, r, st, opts=(), seed=True, scale=None, label=""):
     finally:
         for kk, _ in opts:
             D.set_option(kk, {"ws_mt": 0, "ws_epi_groups": 1, "splits": 0, "pair": 0, "pair_min_kb": 16,
-                              "shifted_window": 1, "tma_store": 0, "tail_split": 0}[kk])
+                              "shifted_window": 1, "tma_store": 0, "tail_split": 0, "stem_fused": 0,
+                              "splitk_inkernel": 1}[kk])
     print(f"{label:34s} plan a_mode={plan['a_mode']} bm={plan['bm']} bn={plan['bn']} splits={plan['splits']} "
           f"{'OK' if ok else 'MISMATCH'}", flush=True)
     return ok
@@ -54,9 +55,13 @@ def main():
     ok &= conv(2, 18, 64, 64, 3, 1, label="conv_ws MT1")
     ok &= conv(3, 18, 64, 64, 3, 1, opts=[("ws_mt", 2)], seed=False, scale=2.0 ** -12, label="conv_ws MT2 requant")
     ok &= conv(3, 18, 64, 64, 3, 1, opts=[("ws_mt", 4), ("ws_epi_groups", 2)], label="conv_ws MT4 EG2")
-    ok &= conv(1, 38, 3, 64, 7, 2, seed=False, scale=2.0 ** -11, label="s2d stem pair MT auto")
-    ok &= conv(1, 38, 3, 64, 7, 2, opts=[("ws_mt", 4)], label="s2d stem pair MT4")
-    ok &= conv(2, 10, 256, 128, 3, 1, opts=[("splits", 3)], label="split-K + fix-up")
+    ok &= conv(2, 62, 3, 64, 7, 2, seed=False, scale=2.0 ** -11, label="s2d stem pair MT auto")
+    ok &= conv(2, 62, 3, 64, 7, 2, opts=[("ws_mt", 4)], label="s2d stem pair MT4")
+    ok &= conv(2, 62, 3, 64, 7, 2, opts=[("stem_fused", 1)], label="fused stem (stem_ws)")
+    ok &= conv(3, 61, 3, 128, 7, 2, opts=[("stem_fused", 1)], seed=False, scale=2.0 ** -11,
+               label="fused stem odd extent requant")
+    ok &= conv(2, 10, 256, 128, 3, 1, opts=[("splits", 3), ("splitk_inkernel", 0)], label="split-K + fix-up kernel")
+    ok &= conv(2, 10, 256, 128, 3, 1, opts=[("splits", 3)], label="split-K, in-kernel fix-up")
     ok &= conv(2, 10, 256, 256, 3, 1, opts=[("shifted_window", 0), ("pair", 1), ("pair_min_kb", 1)],
                seed=False, scale=2.0 ** -13, label="conv_tc2 CTA pair")
     ok &= conv(2, 10, 64, 256, 1, 1, opts=[("shifted_window", 0), ("tma_store", 1)], seed=False,
