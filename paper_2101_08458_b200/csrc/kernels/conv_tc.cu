@@ -936,6 +936,7 @@ void fill_epilogue(ConvKernelParams* pp, const Problem& pb, const Options& o, co
     int ex = 0;
     const float fr = std::frexp(ep.scale, &ex);  // scale = fr * 2^ex, fr in [0.5, 1)
     if (fr == 0.5f && ex - 1 <= 0 && ex - 1 >= -24) p.pow2_k = -(ex - 1);
+    if (p.pow2_k >= 0) p.pow2_mul24 = 1u << (24 - p.pow2_k);
   }
   p.simple = (ep.kind == tzcdev::EP_REQUANT_I8 && p.pow2_k >= 2 && !p.range_check && seed == nullptr && p.vec_ok &&
               pb.out.nb == pb.ngemm)

@@ -114,6 +114,7 @@ struct alignas(64) ConvKernelParams {
   int32_t ep_kind;
   float scale;
   int32_t pow2_k;       // scale == 2^-pow2_k exactly (>= 0), else -1
+  uint32_t pow2_mul24;  // 2^(24 - pow2_k) when 0 <= pow2_k <= 24 (simple requant path)
   int32_t vec_ok;       // 16-column output/seed pieces are 16-byte aligned
   int32_t range_check;  // 0 when |seed + sum| < 2^24 is guaranteed (no seed, K*255*128 < 2^24)
   // shifted-window (weight-stationary) mode: padded pixel grid geometry
@@ -431,15 +432,25 @@ struct EpiCfg {
 
 // The bench / serving case in a few instructions per element: requant by
 // 2^-k with no seed and |acc| < 2^24 guaranteed (host-checked), row-major
-// 16-byte-aligned output.  trunc(c / 2^k) = (c + ((c >> 31) >>> (32-k))) >> k.
+// 16-byte-aligned output.  trunc(c / 2^k) = (c + ((c >> 31) & (2^k - 1))) >> k.
+__device__ __forceinline__ uint32_t requant_pow2_byte3(uint32_t c, uint32_t negmask, uint32_t mul24) {
+  uint32_t t, x;
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(t) : "r"((uint32_t)((int32_t)c >> 31)), "r"(negmask), "r"(c));
+  asm("mul.lo.u32 %0, %1, %2;" : "=r"(x) : "r"(t), "r"(mul24));
+  return x;
+}
+
 template <int CW, int BN>
 __device__ __forceinline__ void epi_simple(const ConvKernelParams& p, int m, int n, const uint32_t* v, uint32_t stg,
                                            int srow, int scol) {
-  // trunc(c / 2^k) for |c| < 2^24, k >= 2, spread over both integer pipes:
-  //   s = c >> 31 (ALU SHF), t = c - s*(2^k - 1) (fma-pipe IMAD),
-  //   q = mulhi(t, 2^(32-k)) == t >> k (fma-pipe IMAD.HI), pack (ALU PRMT)
-  const int32_t negmask = -(int32_t)((1u << p.pow2_k) - 1u);
-  const int32_t mul = (int32_t)(1u << (32 - p.pow2_k));
+  // low byte of trunc(c / 2^k) for |c| < 2^24, 2 <= k <= 24, as full-rate
+  // integer ops on both pipes (tools/epi_probe.cu: IMAD.HI runs at half the
+  // IMAD rate and made this loop fma-pipe bound):
+  //   s = c >> 31 (ALU SHF), t = c + s * -(2^k - 1) (IMAD), x = t * 2^(24-k)
+  //   (IMAD, mod 2^32: byte 3 of x = bits [k, k+8) of t), pack byte 3 of four
+  //   x (ALU PRMT).  2 IMAD + 1.75 ALU per element.
+  const uint32_t negmask = (uint32_t)-(int32_t)((1u << p.pow2_k) - 1u);
+  const uint32_t mul24 = p.pow2_mul24;  // 2^(24-k), opaque to the compiler (stays an IMAD)
   int8_t* o = static_cast<int8_t*>(p.out) + (int64_t)m * p.out_stride_m + n;
   if (CW == 32 && !stg && p.vec32 && n + 32 <= p.Ngemm) {
     // one 256-bit store per row chunk: whole 32-byte sectors (no half-sector
@@ -449,11 +460,8 @@ __device__ __forceinline__ void epi_simple(const ConvKernelParams& p, int m, int
     for (int q = 0; q < 8; ++q) {
       uint32_t b[4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int32_t c = (int32_t)v[4 * q + i];
-        b[i] = (uint32_t)__mulhi((c >> 31) * negmask + c, mul);
-      }
-      w[q] = __byte_perm(__byte_perm(b[0], b[1], 0x0040), __byte_perm(b[2], b[3], 0x0040), 0x5410);
+      for (int i = 0; i < 4; ++i) b[i] = requant_pow2_byte3(v[4 * q + i], negmask, mul24);
+      w[q] = __byte_perm(__byte_perm(b[0], b[1], 0x0073), __byte_perm(b[2], b[3], 0x0073), 0x5410);
     }
     st_v8(o, w);
     return;
@@ -463,15 +471,11 @@ __device__ __forceinline__ void epi_simple(const ConvKernelParams& p, int m, int
     if (n + 16 * j >= p.Ngemm) break;  // ragged N: pieces past the last column
     uint32_t b[16];
 #pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      const int32_t c = (int32_t)v[16 * j + i];
-      const int32_t t = (c >> 31) * negmask + c;
-      b[i] = (uint32_t)__mulhi(t, mul);
-    }
+    for (int i = 0; i < 16; ++i) b[i] = requant_pow2_byte3(v[16 * j + i], negmask, mul24);
     uint32_t w[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q)
-      w[q] = __byte_perm(__byte_perm(b[4 * q], b[4 * q + 1], 0x0040), __byte_perm(b[4 * q + 2], b[4 * q + 3], 0x0040),
+      w[q] = __byte_perm(__byte_perm(b[4 * q], b[4 * q + 1], 0x0073), __byte_perm(b[4 * q + 2], b[4 * q + 3], 0x0073),
                          0x5410);
     if (stg)
       st_shared_v4(stage_addr<BN>(stg, srow, scol + 16 * j), w[0], w[1], w[2], w[3]);
