@@ -938,7 +938,7 @@ void fill_epilogue(ConvKernelParams* pp, const Problem& pb, const Options& o, co
     if (fr == 0.5f && ex - 1 <= 0 && ex - 1 >= -24) p.pow2_k = -(ex - 1);
     if (p.pow2_k >= 0) p.pow2_mul24 = 1u << (24 - p.pow2_k);
   }
-  p.simple = (ep.kind == tzcdev::EP_REQUANT_I8 && p.pow2_k >= 2 && !p.range_check && seed == nullptr && p.vec_ok &&
+  p.simple = (ep.kind == tzcdev::EP_REQUANT_I8 && p.pow2_k >= 2 && !pb.f16 && seed == nullptr && p.vec_ok &&
               pb.out.nb == pb.ngemm)
                  ? 1
                  : 0;

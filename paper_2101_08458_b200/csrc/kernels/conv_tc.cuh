@@ -433,16 +433,14 @@ struct EpiCfg {
 // The bench / serving case in a few instructions per element: requant by
 // 2^-k with no seed and |acc| < 2^24 guaranteed (host-checked), row-major
 // 16-byte-aligned output.  trunc(c / 2^k) = (c + ((c >> 31) & (2^k - 1))) >> k.
-__device__ __forceinline__ uint32_t requant_pow2_byte3(uint32_t c, uint32_t negmask, uint32_t mul24) {
-  uint32_t t, x;
-  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(t) : "r"((uint32_t)((int32_t)c >> 31)), "r"(negmask), "r"(c));
-  asm("mul.lo.u32 %0, %1, %2;" : "=r"(x) : "r"(t), "r"(mul24));
-  return x;
-}
-
-template <int CW, int BN>
-__device__ __forceinline__ void epi_simple(const ConvKernelParams& p, int m, int n, const uint32_t* v, uint32_t stg,
-                                           int srow, int scol) {
+// kChk (K * 255 * 128 >= 2^24, so |c| < 2^24 is not guaranteed): every
+// element also ORs |c| - (c < 0) into one word (one LOP3); a lane whose chunk
+// saw |c| >= 2^24 (rare: the fp32 cast rounds there) redoes that chunk with the
+// exact RNE24 form.  The check costs one ALU op per element instead of the
+// general path's conversion-free but longer sequence.
+template <int CW, int BN, bool kChk>
+__device__ __forceinline__ void epi_simple_impl(const ConvKernelParams& p, int m, int n, const uint32_t* v,
+                                                uint32_t stg, int srow, int scol) {
   // low byte of trunc(c / 2^k) for |c| < 2^24, 2 <= k <= 24, as full-rate
   // integer ops on both pipes (tools/epi_probe.cu: IMAD.HI runs at half the
   // IMAD rate and made this loop fma-pipe bound):
@@ -452,6 +450,23 @@ __device__ __forceinline__ void epi_simple(const ConvKernelParams& p, int m, int
   const uint32_t negmask = (uint32_t)-(int32_t)((1u << p.pow2_k) - 1u);
   const uint32_t mul24 = p.pow2_mul24;  // 2^(24-k), opaque to the compiler (stays an IMAD)
   int8_t* o = static_cast<int8_t*>(p.out) + (int64_t)m * p.out_stride_m + n;
+  uint32_t big = 0;
+  auto byte3 = [&](uint32_t c) -> uint32_t {
+    const uint32_t s = (uint32_t)((int32_t)c >> 31);
+    if constexpr (kChk) big |= c ^ s;
+    uint32_t t, x;
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(t) : "r"(s), "r"(negmask), "r"(c));
+    asm("mul.lo.u32 %0, %1, %2;" : "=r"(x) : "r"(t), "r"(mul24));
+    return x;
+  };
+  auto exact3 = [&](uint32_t c) -> uint32_t {  // RNE24 cast, then trunc(/ 2^k), at byte 3
+    const bool neg = (int32_t)c < 0;
+    const uint32_t mq = rne24(neg ? 0u - c : c) >> p.pow2_k;
+    return (neg ? 0u - mq : mq) << 24;
+  };
+  auto pack = [](const uint32_t* b) {
+    return __byte_perm(__byte_perm(b[0], b[1], 0x0073), __byte_perm(b[2], b[3], 0x0073), 0x5410);
+  };
   if (CW == 32 && !stg && p.vec32 && n + 32 <= p.Ngemm) {
     // one 256-bit store per row chunk: whole 32-byte sectors (no half-sector
     // L2 writes) and half the store instructions
@@ -460,8 +475,17 @@ __device__ __forceinline__ void epi_simple(const ConvKernelParams& p, int m, int
     for (int q = 0; q < 8; ++q) {
       uint32_t b[4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) b[i] = requant_pow2_byte3(v[4 * q + i], negmask, mul24);
-      w[q] = __byte_perm(__byte_perm(b[0], b[1], 0x0073), __byte_perm(b[2], b[3], 0x0073), 0x5410);
+      for (int i = 0; i < 4; ++i) b[i] = byte3(v[4 * q + i]);
+      w[q] = pack(b);
+    }
+    if (kChk && big >= (1u << 24)) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        uint32_t b[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) b[i] = exact3(v[4 * q + i]);
+        w[q] = pack(b);
+      }
     }
     st_v8(o, w);
     return;
@@ -469,19 +493,38 @@ __device__ __forceinline__ void epi_simple(const ConvKernelParams& p, int m, int
 #pragma unroll
   for (int j = 0; j < CW / 16; ++j) {
     if (n + 16 * j >= p.Ngemm) break;  // ragged N: pieces past the last column
-    uint32_t b[16];
-#pragma unroll
-    for (int i = 0; i < 16; ++i) b[i] = requant_pow2_byte3(v[16 * j + i], negmask, mul24);
     uint32_t w[4];
+    big = 0;
 #pragma unroll
-    for (int q = 0; q < 4; ++q)
-      w[q] = __byte_perm(__byte_perm(b[4 * q], b[4 * q + 1], 0x0073), __byte_perm(b[4 * q + 2], b[4 * q + 3], 0x0073),
-                         0x5410);
+    for (int q = 0; q < 4; ++q) {
+      uint32_t b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) b[i] = byte3(v[16 * j + 4 * q + i]);
+      w[q] = pack(b);
+    }
+    if (kChk && big >= (1u << 24)) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        uint32_t b[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) b[i] = exact3(v[16 * j + 4 * q + i]);
+        w[q] = pack(b);
+      }
+    }
     if (stg)
       st_shared_v4(stage_addr<BN>(stg, srow, scol + 16 * j), w[0], w[1], w[2], w[3]);
     else
       st_v4(o + 16 * j, w[0], w[1], w[2], w[3]);
   }
+}
+
+template <int CW, int BN>
+__device__ __forceinline__ void epi_simple(const ConvKernelParams& p, int m, int n, const uint32_t* v, uint32_t stg,
+                                           int srow, int scol) {
+  if (p.range_check)
+    epi_simple_impl<CW, BN, true>(p, m, n, v, stg, srow, scol);
+  else
+    epi_simple_impl<CW, BN, false>(p, m, n, v, stg, srow, scol);
 }
 
 // One tcgen05.ld chunk of CW accumulator columns for row m (m < 0: no row).

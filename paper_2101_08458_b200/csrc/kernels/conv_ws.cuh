@@ -240,7 +240,7 @@ __global__ void __launch_bounds__(EpiCfg<BN>::THREADS, 1) conv_ws_kernel(const _
           const bool fast = p.vec_ok && BN <= p.Ngemm;
           if (cols == 16) {
             epi_chunk<16, kF16, kEpm, BN>(p, tq, m, col0, fast);
-          } else if (kEpm == EPM_REQUANT && p.simple && cols == 64) {
+          } else if (kEpm == EPM_REQUANT && p.simple && !p.range_check && cols == 64) {
             // the bench / serving requant: both 32-column TMEM loads in flight
             // before one wait (the lean simple path leaves room for 64
             // accumulator registers; the general paths keep one chunk)
@@ -249,8 +249,8 @@ __global__ void __launch_bounds__(EpiCfg<BN>::THREADS, 1) conv_ws_kernel(const _
             tmem_ld32(tq + 32, vb);
             tmem_ld_wait();
             if (m >= 0) {
-              epi_simple<32, BN>(p, m, col0, va, 0u, 0, 0);
-              epi_simple<32, BN>(p, m, col0 + 32, vb, 0u, 0, 0);
+              epi_simple_impl<32, BN, false>(p, m, col0, va, 0u, 0, 0);
+              epi_simple_impl<32, BN, false>(p, m, col0 + 32, vb, 0u, 0, 0);
             }
           } else {
 #pragma unroll 1

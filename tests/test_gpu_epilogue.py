@@ -127,3 +127,34 @@ def test_wide_stores_f16_and_raw_outputs(cuda, st256):
     hv = h.view(torch.int16).numpy().view(np.uint16).view(np.float16).astype(np.float64)
     assert rel_dev(Orc.conv2d_nhwc(x, w, 1, fp16=True), hv) <= 1e-3 + 2 ** -11
     assert np.array_equal(i32, Orc.matmul(a, b))
+
+
+def extreme_operands(shape_x, shape_w, seed):
+    """Random u8 / i8 operands where the first half of the output channels see
+    all-255 inputs against all -128 / +127 weights somewhere, so accumulators
+    reach |c| >= 2^24 (the fp32 cast rounds: the checked 2^-k path must take
+    its exact RNE24 fallback) next to ordinary ones."""
+    x = Orc.random_tensor("u8", shape_x, seed)
+    w = Orc.random_tensor("i8", shape_w, seed + 1)
+    x = x.copy()
+    w = w.copy()
+    x.reshape(-1, shape_x[-1])[: x.reshape(-1, shape_x[-1]).shape[0] // 3] = 255
+    k = shape_w[0]
+    w[: k // 4] = -128
+    w[k // 4: k // 2] = 127
+    return x, w
+
+
+@pytest.mark.parametrize("c,r,hp", [(1024, 1, 20), (128, 3, 22), (2048, 1, 9)])
+@pytest.mark.parametrize("scale", [2.0 ** -12, 2.0 ** -6])
+def test_simple_requant_checked_large_k(cuda, c, r, hp, scale):
+    """K * 255 * 128 >= 2^24: the 2^-k fast path with its per-chunk |c| check
+    (r = 3, C = 128 runs on the shifted-window kernel, the 1x1 layers on the
+    general one), bit-exact to cast<i8>(cast<fp32>(C) * 2^-k) including the
+    |c| >= 2^24 elements where the fp32 cast rounds."""
+    n, k = 3, 256
+    x, w = extreme_operands((n, hp, hp, c), (k, r, r, c), 700 + c + r)
+    ref = Orc.conv2d_nhwc(x, w, 1)
+    assert np.abs(ref.astype(np.int64)).max() >= (1 << 24)  # the fallback is exercised
+    got = D.conv2d(to_dev(x, cuda), to_dev(w, cuda), 1, epilogue="requant_i8", scale=scale).cpu().numpy()
+    assert np.array_equal(got, Orc.requant_i8(ref, scale))

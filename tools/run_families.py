@@ -37,6 +37,12 @@ def run(name, f16, batch):
     torch.cuda.synchronize()
 
 
+for n in sel:  # explicit layer names
+    if any(L.name == n for L in RESNET50_V15):
+        run(n, False, 256)
+if "suite" in sel:  # all 23 layers of the timed step, in suite order
+    for L in RESNET50_V15:
+        run(L.name, False, 256)
 if "all" in sel or "i8" in sel:
     for n in I8:
         run(n, False, 256)

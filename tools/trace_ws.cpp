@@ -33,6 +33,11 @@ int main(int argc, char** argv) {
   tzc_epilogue ep{TZC_EP_REQUANT_I8, 1.0f / 4096};
   if (argc > 7) tzc_debug_flags(atoi(argv[7]));
   if (argc > 8) tzc_b200_set_option("shifted_window", atoi(argv[8]));
+  // warm the clocks first: a few hundred launches (~50-100 ms) so the traced
+  // launches run at the sustained SM clock, not the idle one (a trace taken
+  // right after start-up ran at ~1 GHz)
+  for (int wu = 0; wu < 400; ++wu) tzc_b200_conv2d_i8(&d, (const uint8_t*)x, (const int8_t*)w, nullptr, o, &ep, nullptr);
+  cudaDeviceSynchronize();
   for (int it = 0; it < 3; ++it) {
     cudaEvent_t a, b;
     cudaEventCreate(&a); cudaEventCreate(&b);
