@@ -641,9 +641,15 @@ __global__ void __launch_bounds__(EpiCfg<BN>::THREADS, 1) conv_tc_kernel(const _
 
   const int num_units = p.full_units + (p.num_tiles - p.full_units) * p.splits;
 
-  if (warp == 0) {
-    // ===================== TMA producer =====================
+  if (warp == 0 || warp == 3) {
+    // ===================== TMA producers =====================
+    // Two producer warps take alternate K blocks (tools/tma_probe.cu: one
+    // issuing thread that waits on its ring between loads completes tiled TMA
+    // loads ~serially, ~26 B/clk/SM for 16 KB boxes; loads issued from
+    // several warps overlap, ~60 B/clk/SM from L2).
     if (lane == 0) {
+      const uint32_t pj = warp == 0 ? 0u : 1u;
+      uint32_t g = 0;  // K blocks seen (both producers walk every block, act on their parity)
       int stage = 0;
       uint32_t phase = 0;
       for (int u = blockIdx.x, it = 0; u < num_units; u += gridDim.x, ++it) {
@@ -658,7 +664,14 @@ __global__ void __launch_bounds__(EpiCfg<BN>::THREADS, 1) conv_tc_kernel(const _
           oh = (int)fdiv(rem, p.fd_ow);
           ow = rem - oh * p.OW;
         }
-        for (int kb = kb0; kb < kb1; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb, ++g) {
+          if ((g & 1u) != pj) {
+            if (++stage == STAGES) {
+              stage = 0;
+              phase ^= 1;
+            }
+            continue;
+          }
           mbar_wait(&empty[stage], phase ^ 1);
           if (kb == kb0 && it < 10) TZC_TRACE_POINT(10 + 5 * it);
           const int tap = (int)fdiv(kb, p.fd_cblocks);
