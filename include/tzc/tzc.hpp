@@ -286,6 +286,9 @@ struct KernelPlan {
   std::string data, weight, out;  // op tensor names bound to a, b, d
   int64_t splits = 0;             // device split-K from the schedule's split_reduction (0 = planner's choice)
   int64_t dp = 1, kd = 1, od = 1; // ConvBlocked3D: input depth, depth taps, output depth
+  // the instruction's tile: M rows per MMA (256 = cta_group::2, the CTA-pair
+  // kernel) and N columns per MMA, which the launch uses as its N tile
+  int64_t tile_m = 128, tile_n = 0;
   std::string describe() const;
 };
 struct Transform;

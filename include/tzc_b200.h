@@ -146,6 +146,21 @@ TZC_API int tzc_b200_gemm_f16(const tzc_gemm_desc* d, const uint16_t* a, const u
                       const float* c_seed, void* out, const tzc_epilogue* ep, void* stream);
 
 TZC_API int tzc_b200_plan_conv(const tzc_conv_desc* d, tzc_plan* plan);
+
+/* What the calling thread's most recent conv/GEMM launch actually ran (the
+ * executed tile, not a plan query): kernel 0 = general (TMA tiled / im2col),
+ * 1 = shifted-window, 2 = space-to-depth stem (shifted-window, pair mode),
+ * 3 = CTA pair (cta_group::2, M = 256 rows per MMA), 4 = K7 GEMM (thin
+ * channels).  Returns TZC_E_SHAPE if this thread has launched nothing. */
+typedef struct tzc_launch_info {
+  int32_t kernel;
+  int32_t cta_group;       /* 1 or 2 */
+  int32_t bm, bn, bk_bytes;
+  int32_t a_mode;
+  int32_t grid;
+  int32_t splits;
+} tzc_launch_info;
+TZC_API int tzc_b200_last_launch(tzc_launch_info* info);
 TZC_API int tzc_b200_plan_gemm(const tzc_gemm_desc* d, tzc_plan* plan);
 /* Force a split-K factor for subsequent launches (0 = automatic). */
 TZC_API int tzc_b200_set_splits(int32_t splits);

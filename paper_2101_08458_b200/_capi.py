@@ -37,7 +37,7 @@ EXPORTS = (
     "tzc_b200_set_problem_options_conv", "tzc_b200_set_problem_options_gemm", "tzc_b200_tune_candidates",
     "tzc_b200_parse", "tzc_b200_inspect", "tzc_b200_describe", "tzc_b200_builtins",
     "tzc_b200_print_intrinsic",
-    "tzc_b200_last_error", "tzc_b200_launch_count", "tzc_b200_device_ok", "tzc_b200_version",
+    "tzc_b200_last_error", "tzc_b200_launch_count", "tzc_b200_last_launch", "tzc_b200_device_ok", "tzc_b200_version",
 )
 
 
@@ -69,6 +69,11 @@ class GemmDesc(C.Structure):
 
 class Epilogue(C.Structure):
     _fields_ = [("kind", C.c_int32), ("scale", C.c_float)]
+
+
+class LaunchInfo(C.Structure):
+    _fields_ = [("kernel", C.c_int32), ("cta_group", C.c_int32), ("bm", C.c_int32), ("bn", C.c_int32),
+                ("bk_bytes", C.c_int32), ("a_mode", C.c_int32), ("grid", C.c_int32), ("splits", C.c_int32)]
 
 
 class Plan(C.Structure):

@@ -251,6 +251,12 @@ const char* tzc_b200_last_error(void) { return g_last_error.c_str(); }
 
 uint64_t tzc_b200_launch_count(void) { return g_launches.load(); }
 
+int tzc_b200_last_launch(tzc_launch_info* info) {
+  if (!info) return report(Status(TZC_E_SHAPE, "null tzc_launch_info"));
+  if (!tzcb200::last_launch(info)) return report(Status(TZC_E_SHAPE, "no launch on this thread yet"));
+  return TZC_OK;
+}
+
 int tzc_b200_device_ok(void) {
   try {
     return device_ok();

@@ -95,7 +95,7 @@ std::string KernelPlan::describe() const {
   os << fam << (f16 ? " f16" : " u8i8") << " n=" << n << " hp=" << hp << " wp=" << wp << " c=" << c << " k=" << k
      << (family == Family::ConvBlocked3D ? " dp=" + std::to_string(dp) + " kd=" + std::to_string(kd) : std::string())
      << " r=" << r << " s=" << s << " stride=" << stride << " m=" << m << (b_kn ? " b_kn" : "") << " out(nb=" << out_nb
-     << ",sm=" << out_stride_m << ",sb=" << out_stride_blk << ")";
+     << ",sm=" << out_stride_m << ",sb=" << out_stride_blk << ") tile=m" << tile_m << "n" << tile_n;
   return os.str();
 }
 
@@ -165,6 +165,8 @@ KernelPlan plan_for(const ComputeOp& op, const Intrinsic& intr, const LoopMappin
 
   KernelPlan p;
   p.f16 = mn.find("kind::f16") != std::string::npos;
+  p.tile_m = il[0].extent;
+  p.tile_n = il[1].extent;
   p.data = A->name;
   p.weight = B->name;
   p.out = op.out;
@@ -627,6 +629,21 @@ Epi epilogue_of(const ComputeOp& main, const ComputeOp* ep) {
 
 }  // namespace
 
+// The instruction's tile binds the launch: N = the instruction's N when it
+// divides the output channels (the printed TensorIR's 64-wide calls run as
+// 64-wide N tiles), M = 256 (cta_group::2) selects the CTA-pair kernel.
+tzcb200::Options instruction_options(const KernelPlan& p, tzcb200::Options o) {
+  const bool flat = p.family == KernelPlan::Family::Matmul || p.family == KernelPlan::Family::ConvNHWC;
+  if (flat && p.tile_n > 0 && p.k % p.tile_n == 0 && (p.tile_n == 64 || p.tile_n == 128 || p.tile_n == 256))
+    o.bn = (int)p.tile_n;
+  if (p.tile_m == 256) {
+    o.pair = 1;
+    o.pair_min_kb = 0;
+    o.shifted_window = 0;
+  }
+  return o;
+}
+
 void run_tensorized_packed(const TensorizedOp& t, const std::map<std::string, const void*>& host, void* host_out,
                            int64_t out_bytes, const ComputeOp* epilogue_op) {
   using namespace tzcb200;
@@ -664,7 +681,7 @@ void run_tensorized_packed(const TensorizedOp& t, const std::map<std::string, co
   ol.stride_m = p.out_stride_m;
   ol.stride_blk = p.out_stride_blk;
   const tzc_epilogue e{ep.kind, ep.scale};
-  const Options opts = options_for("");  // one plan-option snapshot for every launch of this call
+  const Options opts = instruction_options(p, options_for(""));  // one plan-option snapshot for every launch of this call
   auto fail = [](const Status& s) {
     if (s.code == TZC_E_DEVICE) throw DeviceError(s.msg);
     throw InjectError(s.msg);

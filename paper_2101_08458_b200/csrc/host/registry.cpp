@@ -210,20 +210,21 @@ const char* kWmma16 =
 // tcgen05.mma (sm_100a): one CTA-wide MMA, D in TMEM (+= in place), A/B in
 // shared memory.  kind::i8: u8 x s8 -> s32, K = 32 per instruction (256 bits).
 // kind::f16: f16 x f16 -> f32, K = 16.  B K-major (b[n,k]) or MN-major (b[k,n]).
-std::string tcgen05_text(bool f16, int n, bool mn_major) {
+std::string tcgen05_text(bool f16, int n, bool mn_major, int m = 128) {
   const int k = f16 ? 16 : 32;
   const std::string da = f16 ? "fp16" : "u8", db = f16 ? "fp16" : "i8", dd = f16 ? "fp32" : "i32";
   const std::string bshape = mn_major ? "[" + std::to_string(k) + ", " + std::to_string(n) + "]"
                                       : "[" + std::to_string(n) + ", " + std::to_string(k) + "]";
   std::ostringstream os;
-  os << "tensor a : " << da << " [128, " << k << "] input\n"
+  os << "tensor a : " << da << " [" << m << ", " << k << "] input\n"
      << "tensor b : " << db << " " << bshape << " input\n"
-     << "tensor d : " << dd << " [128, " << n << "] output\n"
-     << "loop m : dp 128\nloop n : dp " << n << "\nloop k : red " << k << "\n"
+     << "tensor d : " << dd << " [" << m << ", " << n << "] output\n"
+     << "loop m : dp " << m << "\nloop n : dp " << n << "\nloop k : red " << k << "\n"
      << "d[m, n] += cast<" << dd << ">(a[m, k]) * cast<" << dd << ">(" << (mn_major ? "b[k, n]" : "b[n, k]") << ")\n"
      << "rule a: vectorize(k) unroll_concat(m)\n"
      << (mn_major ? "rule b: vectorize(n) unroll_concat(k)\n" : "rule b: vectorize(k) unroll_concat(n)\n")
-     << "mnemonic \"tcgen05.mma.cta_group::1.kind::" << (f16 ? "f16" : "i8") << " m128n" << n << "k" << k
+     << "mnemonic \"tcgen05.mma.cta_group::" << (m == 256 ? 2 : 1) << ".kind::" << (f16 ? "f16" : "i8") << " m" << m
+     << "n" << n << "k" << k
      << (mn_major ? " b.mn_major" : "") << "\"\n";
   return os.str();
 }
@@ -240,6 +241,12 @@ const std::map<std::string, Intrinsic>& table() {
       m.emplace("tcgen05_f16_m128n" + ns + "k16", parse_intrinsic(tcgen05_text(true, n, false), "tcgen05_f16_m128n" + ns + "k16"));
       m.emplace("tcgen05_f16_m128n" + ns + "k16_mn",
                 parse_intrinsic(tcgen05_text(true, n, true), "tcgen05_f16_m128n" + ns + "k16_mn"));
+    }
+    // cta_group::2: one MMA over a CTA pair's 256 rows (conv_tc2.cuh; each
+    // CTA loads its 128 A rows and half of B)
+    for (int n : {128, 256}) {
+      const std::string nm = "tcgen05_i8_m256n" + std::to_string(n) + "k32";
+      m.emplace(nm, parse_intrinsic(tcgen05_text(false, n, false, 256), nm));
     }
     return m;
   }();

@@ -113,6 +113,17 @@ using tzcdev::ConvCfg;
 using tzcdev::ConvKernelParams;
 
 std::atomic<uint64_t> g_launches{0};
+thread_local tzc_launch_info g_last_launch{};
+thread_local bool g_have_last_launch = false;
+void note_launch(int kernel, int cta_group, int bm, int bn, int bk, int a_mode, int grid, int splits) {
+  g_last_launch = tzc_launch_info{kernel, cta_group, bm, bn, bk, a_mode, grid, splits};
+  g_have_last_launch = true;
+}
+bool last_launch(tzc_launch_info* out) {
+  if (!g_have_last_launch) return false;
+  *out = g_last_launch;
+  return true;
+}
 
 namespace {
 
@@ -236,6 +247,7 @@ Status launch_kernel(const ConvKernelParams& p, int grid, cudaStream_t stream) {
   const int smem = ring_smem(BN, KB, p.tma_store ? p.epi_groups : 0, p.stages);  // staging only for TMA stores
   cudaError_t e = launch_pdl(kern, dim3(grid), dim3(tzcdev::EpiCfg<BN>::THREADS), smem, stream, p);
   g_launches.fetch_add(1, std::memory_order_relaxed);
+  note_launch(0, 1, 128, BN, KB, AM, grid, p.splits);
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) return Status(TZC_E_DEVICE, std::string("conv_tc launch: ") + cudaGetErrorString(e));
   return Status();
@@ -270,6 +282,7 @@ Status launch_pair(const ConvKernelParams& p, int grid, cudaStream_t stream) {
 #endif
   cudaError_t e = cudaLaunchKernelEx(&cfg, kern, p);
   g_launches.fetch_add(1, std::memory_order_relaxed);
+  note_launch(3, 2, 256, BN, 128, AM, grid, 1);
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) return Status(TZC_E_DEVICE, std::string("conv_tc2 launch: ") + cudaGetErrorString(e));
   return Status();
@@ -570,6 +583,7 @@ Status launch_ws_kernel(const ConvKernelParams& p, int grid, int smem, cudaStrea
   if (!sa.ok()) return sa;
   cudaError_t e = launch_pdl(kern, dim3(grid), dim3(tzcdev::EpiCfg<BN>::THREADS), smem, stream, p);
   g_launches.fetch_add(1, std::memory_order_relaxed);
+  note_launch(PAIR ? 2 : 1, 1, 128 * p.mt, BN, KB, PAIR ? 3 : 2, grid, 1);
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) return Status(TZC_E_DEVICE, std::string("conv_ws launch: ") + cudaGetErrorString(e));
   return Status();
@@ -609,6 +623,7 @@ WsFn ws_fn(int bn, int kb, bool f16, bool pair) {
 // (pair = 16-byte pixels, the space-to-depth stem).
 bool ws_plan(const Problem& pb, bool pair, const Options& o, WsPlan* w) {
   if (pb.b_kn || pb.stride != 1 || needs_k7(pb)) return false;
+  if (o.bn && o.bn != pb.ngemm) return false;  // a narrower N tile (the instruction's N) runs on the general kernel
   // 1x1: weight-stationary pays off only for a single 64-wide N tile and one
   // K block (c2_1x1_64_64: 43 -> 31 us at batch 256); wider layers keep the
   // TMA-store general kernel (measured, tools/layer_timing.py --opt ws_1x1=1)
@@ -781,6 +796,7 @@ Status launch_stem(const ConvKernelParams& p, int grid, int smem, cudaStream_t s
   if (!sa.ok()) return sa;
   cudaError_t e = launch_pdl(kern, dim3(grid), dim3(tzcdev::EpiCfg<BN>::THREADS), smem, stream, p);
   g_launches.fetch_add(1, std::memory_order_relaxed);
+  note_launch(2, 1, 128 * p.mt, BN, 16, 3, grid, 1);
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) return Status(TZC_E_DEVICE, std::string("stem_ws launch: ") + cudaGetErrorString(e));
   return Status();
@@ -991,7 +1007,9 @@ Status run_problem(const Problem& pb, const Options& o, const void* a, const voi
     if (st.ok()) st = im2col_pad(pb, a, wa, kp, stream);
     if (st.ok()) st = weight_pad(pb, b, wb, kp, stream);
     if (!st.ok()) return st;
-    return run_problem(g, o, wa, wb, seed, out, ep, stream);
+    st = run_problem(g, o, wa, wb, seed, out, ep, stream);
+    if (st.ok()) g_last_launch.kernel = 4;  // the thin-channel GEMM rewrite
+    return st;
   }
   tzc_plan plan;
   st = plan_problem(pb, o, &plan);

@@ -100,6 +100,8 @@ Status s2d_stem(const Problem& pb, const void* x, const void* w, void* x4, void*
                 cudaStream_t st);
 
 extern std::atomic<uint64_t> g_launches;
+// the calling thread's most recent launch (tzc_b200_last_launch)
+bool last_launch(tzc_launch_info* out);
 void set_last_error(const std::string& msg);
 
 }  // namespace tzcb200

@@ -174,3 +174,17 @@ def set_option(name: str, value: int):
 
 def launch_count() -> int:
     return int(lib().tzc_b200_launch_count())
+
+
+LAUNCH_KERNELS = {0: "general", 1: "shifted_window", 2: "s2d_stem", 3: "cta_pair", 4: "k7_gemm"}
+
+
+def last_launch() -> dict:
+    """The executed tile of this thread's most recent conv / GEMM launch
+    (tzc_b200_last_launch): kernel family, cta_group, bm, bn, bk_bytes, ..."""
+    from ._capi import LaunchInfo
+    info = LaunchInfo()
+    check(lib().tzc_b200_last_launch(C.byref(info)))
+    out = {f: getattr(info, f) for f, _ in LaunchInfo._fields_}
+    out["kernel"] = LAUNCH_KERNELS.get(out["kernel"], str(out["kernel"]))
+    return out

@@ -268,3 +268,48 @@ def test_resnet18_3d_bank_on_device(cuda, shape):
         w = kern[ko, :, :, :, :, ki, :].astype(np.int64)
         want = np.int64((x * w).sum()).astype(np.int32)
         assert out[ko, od, oh, ow, ki] == want, (ko, od, oh, ow, ki)
+
+
+@pytest.mark.parametrize("n", [64, 128, 256])
+@pytest.mark.parametrize("form", ["matmul", "conv3x3", "conv1x1"])
+def test_instruction_n_is_the_executed_tile(cuda, n, form):
+    """The selected tcgen05 description's N is the N tile the launch runs
+    (it used to be advisory), for the general and the
+    shifted-window kernels alike; results stay bit-exact."""
+    from paper_2101_08458_b200 import device as D
+    if form == "matmul":
+        text = matmul_tdsl(384, 256, 192)
+        ins = Orc.random_inputs(decls(text), 90)
+        ref = Orc.matmul(ins["A"], ins["B"], ins["C"])
+    else:
+        r = 3 if form == "conv3x3" else 1
+        text = conv2d_nhwc_tdsl(2, 14, 14, 64, 256, r, r, 1)
+        ins = Orc.random_inputs(decls(text), 91)
+        ref = Orc.conv2d_nhwc(ins["data"], ins["kernel"], 1, ins["out"])
+    got = ops.run_op(text, f"tcgen05_i8_m128n{n}k32", ins)
+    info = D.last_launch()
+    assert info["bn"] == n and info["cta_group"] == 1, info
+    assert np.array_equal(got, ref)
+
+
+@pytest.mark.parametrize("n", [128, 256])
+@pytest.mark.parametrize("form", ["matmul", "conv3x3"])
+def test_m256_instruction_runs_the_cta_pair_kernel(cuda, n, form):
+    """tcgen05_i8_m256n{N}k32 (cta_group::2): the fused-requant op runs on the
+    CTA-pair kernel (256 rows per MMA, each CTA loads half of B), bit-exact."""
+    from paper_2101_08458_b200 import device as D
+    if form == "matmul":
+        text = matmul_tdsl(768, 256, 512)
+        ins = Orc.random_inputs(decls(text), 92)
+        ref = Orc.matmul(ins["A"], ins["B"], ins["C"])
+        shape = (768, 256)
+        epi = requant_tdsl(shape, 2.0 ** -14)
+    else:
+        text = conv2d_nhwc_tdsl(2, 16, 16, 128, 256, 3, 3, 1)
+        ins = Orc.random_inputs(decls(text), 93)
+        ref = Orc.conv2d_nhwc(ins["data"], ins["kernel"], 1, ins["out"])
+        epi = requant_tdsl(ref.shape, 2.0 ** -14, src="out")
+    q = ops.run_op(text, f"tcgen05_i8_m256n{n}k32", ins, epilogue=epi)
+    info = D.last_launch()
+    assert info["kernel"] == "cta_pair" and info["cta_group"] == 2 and info["bm"] == 256 and info["bn"] == n, info
+    assert np.array_equal(q, Orc.requant_i8(ref, 2.0 ** -14))
