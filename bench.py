@@ -64,6 +64,9 @@ def parse():
                          "-1 (auto) = 2 when a rank holds <= 64 images (layers leave SMs idle, plans matter), "
                          "else 0 (at 256 the search kept every default in 3/3 runs and only heated the GPU)")
     ap.add_argument("--tune-reps", type=int, default=20)
+    ap.add_argument("--save-plans", default="",
+                    help="after the plan search, write the installed per-layer plans to this plan-cache file "
+                         "(tzc_b200_save_tuning; load it with TZC_B200_PLAN_CACHE=<file> or tzc_b200_load_tuning)")
     ap.add_argument("--branch-search", type=int, default=1,
                     help="1: choose the layer-to-branch assignment by measured step time before timing")
     ap.add_argument("--no-e2e", action="store_true")
@@ -423,6 +426,8 @@ def run_ours(args, rank, world, local):
             suite(False)
             suite_branches()
         torch.cuda.synchronize()
+    if args.save_plans and rank == 0:
+        D.save_tuning(args.save_plans)
         time.sleep(2.0)  # let the power controller settle after the search's back-to-back replays
     if args.branch_search:
         sched.update(branch_search(torch, bufs, stream, flush, suite, suite_branches, sched, rt, evs, order))

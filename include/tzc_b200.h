@@ -223,6 +223,13 @@ TZC_API int tzc_b200_clear_tuning(void);
  * --tune 2) applies its per-layer choices. */
 TZC_API int tzc_b200_set_problem_options_conv(const tzc_conv_desc* d, const char* spec);
 TZC_API int tzc_b200_set_problem_options_gemm(const tzc_gemm_desc* d, const char* spec);
+/* The plan cache on disk: writes every installed per-descriptor plan (tuned or
+ * set) to `path`, one line each, or installs the plans a saved file holds
+ * (all lines are validated before any is installed).  `count` (nullable)
+ * receives the number of plans.  A process started with
+ * TZC_B200_PLAN_CACHE=<path> loads that file before its first launch. */
+TZC_API int tzc_b200_save_tuning(const char* path, int32_t* count);
+TZC_API int tzc_b200_load_tuning(const char* path, int32_t* count);
 /* The candidate option specs tzc_b200_tune_* times, one per line (line 0 = default). */
 TZC_API int tzc_b200_tune_candidates(char* buf, int64_t buflen);
 

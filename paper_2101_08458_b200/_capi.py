@@ -35,6 +35,7 @@ EXPORTS = (
     "tzc_b200_tensor_text", "tzc_b200_tensor_roundtrip",
     "tzc_b200_tune_conv", "tzc_b200_tune_gemm", "tzc_b200_clear_tuning",
     "tzc_b200_set_problem_options_conv", "tzc_b200_set_problem_options_gemm", "tzc_b200_tune_candidates",
+    "tzc_b200_save_tuning", "tzc_b200_load_tuning",
     "tzc_b200_parse", "tzc_b200_inspect", "tzc_b200_describe", "tzc_b200_builtins",
     "tzc_b200_print_intrinsic",
     "tzc_b200_last_error", "tzc_b200_launch_count", "tzc_b200_last_launch", "tzc_b200_device_ok", "tzc_b200_version",

@@ -404,6 +404,26 @@ int tzc_b200_set_problem_options_gemm(const tzc_gemm_desc* d, const char* spec) 
   TZC_GUARD_END
 }
 
+int tzc_b200_save_tuning(const char* path, int32_t* count) {
+  TZC_GUARD_BEGIN
+  if (!path) return report(Status(TZC_E_MISSING_INPUT, "NULL path"));
+  int n = 0;
+  Status st = save_problem_options(path, &n);
+  if (st.ok() && count) *count = n;
+  return report(st);
+  TZC_GUARD_END
+}
+
+int tzc_b200_load_tuning(const char* path, int32_t* count) {
+  TZC_GUARD_BEGIN
+  if (!path) return report(Status(TZC_E_MISSING_INPUT, "NULL path"));
+  int n = 0;
+  Status st = load_problem_options(path, &n);
+  if (st.ok() && count) *count = n;
+  return report(st);
+  TZC_GUARD_END
+}
+
 // The tuner's candidate plans, one option spec per line (line 0 = default = "").
 int tzc_b200_tune_candidates(char* buf, int64_t buflen) {
   std::string s;

@@ -6,9 +6,13 @@
 // copies the defaults and applies the descriptor's overrides under one lock,
 // and the resulting Options value is passed down through plan_problem /
 // run_problem.  Options choose the kernel plan only, never the results.
+#include <cstdio>
 #include <cstdlib>
 #include <map>
+#include <cstring>
+#include <fstream>
 #include <mutex>
+#include <sstream>
 #include <string>
 #include <utility>
 #include <vector>
@@ -90,7 +94,23 @@ const char* const* option_names() {
   return names.data();
 }
 
+Status load_problem_options(const std::string& path, int* count);
+namespace {
+std::once_flag g_cache_once;
+// TZC_B200_PLAN_CACHE=<file>: install a saved plan cache before the first launch
+void autoload_plan_cache() {
+  std::call_once(g_cache_once, [] {
+    const char* path = std::getenv("TZC_B200_PLAN_CACHE");
+    if (!path || !*path) return;
+    int n = 0;
+    Status st = load_problem_options(path, &n);
+    if (!st.ok()) std::fprintf(stderr, "tzc_b200: TZC_B200_PLAN_CACHE not loaded: %s\n", st.msg.c_str());
+  });
+}
+}  // namespace
+
 Options options_for(const std::string& key) {
+  autoload_plan_cache();
   std::lock_guard<std::mutex> lk(g_mu);
   Options o = g_defaults;
   if (!key.empty()) {
@@ -152,6 +172,98 @@ Status set_problem_options(const std::string& key, const std::string& spec) {
 void clear_problem_options() {
   std::lock_guard<std::mutex> lk(g_mu);
   g_problem.clear();
+}
+
+// ---- the plan cache on disk ----------------------------------------------------
+// One installed problem per line: "<kind><hex descriptor bytes> <spec>" where
+// kind is 'c' (tzc_conv_desc) or 'g' (tzc_gemm_desc), followed by a readable
+// "# ..." summary of the descriptor; '#' lines are comments.  The SURVEY's
+// text plan cache: a tuned suite is saved once and every later process (or
+// the CLI) loads it instead of searching again.
+namespace {
+std::string hex_of(const std::string& raw) {
+  static const char* h = "0123456789abcdef";
+  std::string s;
+  for (unsigned char c : raw) {
+    s += h[c >> 4];
+    s += h[c & 15];
+  }
+  return s;
+}
+bool unhex(const std::string& s, std::string* out) {
+  if (s.size() % 2) return false;
+  auto v = [](char c) { return c >= '0' && c <= '9' ? c - '0' : c >= 'a' && c <= 'f' ? c - 'a' + 10 : -1; };
+  out->clear();
+  for (size_t i = 0; i < s.size(); i += 2) {
+    const int a = v(s[i]), b = v(s[i + 1]);
+    if (a < 0 || b < 0) return false;
+    out->push_back((char)(a * 16 + b));
+  }
+  return true;
+}
+std::string summary_of(const std::string& key) {
+  std::ostringstream os;
+  if (key[0] == 'c' && key.size() == 1 + sizeof(tzc_conv_desc)) {
+    tzc_conv_desc c;
+    std::memcpy(&c, key.data() + 1, sizeof(c));
+    os << "conv " << (c.profile == TZC_PROFILE_F16 ? "f16" : "u8i8") << " n=" << c.n << " hp=" << c.hp << " wp=" << c.wp
+       << " c=" << c.c << " k=" << c.k << " r=" << c.r << " s=" << c.s << " stride=" << c.stride;
+  } else if (key[0] == 'g' && key.size() == 1 + sizeof(tzc_gemm_desc)) {
+    tzc_gemm_desc g;
+    std::memcpy(&g, key.data() + 1, sizeof(g));
+    os << "gemm " << (g.profile == TZC_PROFILE_F16 ? "f16" : "u8i8") << " m=" << g.m << " n=" << g.n << " k=" << g.k;
+  }
+  return os.str();
+}
+}  // namespace
+
+Status save_problem_options(const std::string& path, int* count) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  std::ofstream f(path);
+  if (!f) return Status(TZC_E_IO, "cannot write plan cache '" + path + "'");
+  f << "# tzc_b200 plan cache v1: <kind+descriptor hex> <options>  # descriptor\n";
+  int n = 0;
+  for (const auto& [key, items] : g_problem) {
+    std::string spec;
+    for (const auto& [name, v] : items) spec += (spec.empty() ? "" : ";") + name + "=" + std::to_string(v);
+    f << key[0] << hex_of(key.substr(1)) << " " << spec << "  # " << summary_of(key) << "\n";
+    ++n;
+  }
+  if (!f) return Status(TZC_E_IO, "writing plan cache '" + path + "' failed");
+  if (count) *count = n;
+  return Status();
+}
+
+Status load_problem_options(const std::string& path, int* count) {
+  std::ifstream f(path);
+  if (!f) return Status(TZC_E_IO, "cannot read plan cache '" + path + "'");
+  std::string line;
+  int n = 0, lineno = 0;
+  std::vector<std::pair<std::string, std::string>> entries;
+  while (std::getline(f, line)) {
+    ++lineno;
+    const size_t hash = line.find('#');
+    if (hash != std::string::npos) line = line.substr(0, hash);
+    std::istringstream is(line);
+    std::string k, spec;
+    if (!(is >> k)) continue;
+    is >> spec;
+    std::string raw;
+    const size_t want = k[0] == 'c' ? sizeof(tzc_conv_desc) : k[0] == 'g' ? sizeof(tzc_gemm_desc) : 0;
+    if (!want || !unhex(k.substr(1), &raw) || raw.size() != want)
+      return Status(TZC_E_VALIDATION, path + ":" + std::to_string(lineno) + ": bad descriptor key");
+    Options probe;
+    Status st = parse_option_spec(spec, &probe, nullptr);
+    if (!st.ok()) return Status(TZC_E_VALIDATION, path + ":" + std::to_string(lineno) + ": " + st.msg);
+    entries.emplace_back(std::string(1, k[0]) + raw, spec);
+  }
+  for (const auto& [key, spec] : entries) {  // all lines valid: install them
+    Status st = set_problem_options(key, spec);
+    if (!st.ok()) return st;
+    ++n;
+  }
+  if (count) *count = n;
+  return Status();
 }
 
 }  // namespace tzcb200

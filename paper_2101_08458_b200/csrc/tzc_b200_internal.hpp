@@ -76,6 +76,9 @@ Options options_for(const std::string& key);
 Status parse_option_spec(const std::string& spec, Options* o, std::vector<std::pair<std::string, int64_t>>* items);
 Status set_default_option(const std::string& name, int64_t value);
 Status set_problem_options(const std::string& key, const std::string& spec);
+// the plan cache file (one line per installed descriptor)
+Status save_problem_options(const std::string& path, int* count);
+Status load_problem_options(const std::string& path, int* count);
 void clear_problem_options();
 
 Status plan_problem(const Problem& pb, const Options& o, tzc_plan* plan);

@@ -151,6 +151,20 @@ def clear_tuning():
     check(lib().tzc_b200_clear_tuning())
 
 
+def save_tuning(path: str) -> int:
+    """Write every installed per-descriptor plan to the plan-cache file `path`."""
+    n = C.c_int32(0)
+    check(lib().tzc_b200_save_tuning(str(path).encode(), C.byref(n)))
+    return n.value
+
+
+def load_tuning(path: str) -> int:
+    """Install the plans a saved plan-cache file holds; returns how many."""
+    n = C.c_int32(0)
+    check(lib().tzc_b200_load_tuning(str(path).encode(), C.byref(n)))
+    return n.value
+
+
 def unblock_data(src, c, h, w, cb, stream=None):
     dst = torch.empty((1, h, w, c), dtype=src.dtype, device=src.device)
     check(lib().tzc_b200_unblock_data(_ptr(src), _ptr(dst), c, h, w, cb, src.element_size(), _stream(stream)))

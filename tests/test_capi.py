@@ -130,3 +130,32 @@ def test_problem_options_validation_and_candidates():
     with pytest.raises(TzcError, match="unknown option"):
         D.set_conv_plan((2, 10, 10, 64), (64, 3, 3, 64), 1, spec="warp_speed=9")
     D.clear_tuning()
+
+
+def test_plan_cache_save_load_roundtrip(tmp_path):
+    """The text plan cache: installed per-descriptor plans are written one line
+    per descriptor, cleared, loaded back (validated first), and a malformed
+    file is refused without installing anything."""
+    from paper_2101_08458_b200 import device as D
+    D.clear_tuning()
+    D.set_conv_plan((32, 58, 58, 64), (64, 3, 3, 64), 1, spec="ws_mt=2;ws_epi_groups=2")
+    D.set_conv_plan((32, 30, 30, 256), (256, 3, 3, 256), 1, spec="splits=2")
+    path = tmp_path / "plans.txt"
+    assert D.save_tuning(path) == 2
+    text = path.read_text()
+    assert "ws_mt=2;ws_epi_groups=2" in text and "conv u8i8 n=32 hp=58" in text
+    D.clear_tuning()
+    assert D.save_tuning(tmp_path / "empty.txt") == 0
+    assert D.load_tuning(path) == 2
+    assert D.save_tuning(tmp_path / "again.txt") == 2
+    assert (tmp_path / "again.txt").read_text() == text
+    bad = tmp_path / "bad.txt"
+    bad.write_text(text + "cdeadbeef ws_mt=2\n")
+    D.clear_tuning()
+    with pytest.raises(Exception, match="bad descriptor key"):
+        D.load_tuning(bad)
+    assert D.save_tuning(tmp_path / "none.txt") == 0  # nothing installed from the bad file
+    bad.write_text(text.replace("ws_mt=2", "ws_mt=3"))
+    with pytest.raises(Exception, match="illegal value"):
+        D.load_tuning(bad)
+    D.clear_tuning()
