@@ -51,6 +51,7 @@ const Knob kKnobs[] = {
     {"st256", &Options::st256, 0, 1, nullptr},
     {"l2_hints", &Options::l2_hints, 0, 3, nullptr},
     {"tma_store", &Options::tma_store, 0, 2, nullptr},
+    {"b_res", &Options::b_res, 0, 1, nullptr},
     {"stem_fused", &Options::stem_fused, 0, 1, nullptr},
 };
 

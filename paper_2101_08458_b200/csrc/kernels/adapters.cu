@@ -11,6 +11,7 @@
 #include <cstdint>
 
 #include "../tzc_b200_internal.hpp"
+#include "ptx.cuh"
 
 namespace tzcdev {
 
@@ -264,6 +265,87 @@ __global__ void s2d_rows_c3_kernel(const uint8_t* __restrict__ x, uint4* __restr
   }
 }
 
+// The int8 C = 3 stem in ONE launch: the first blocks rearrange the weights
+// (s2d_weight_kernel's work, one launch fewer on the stem's critical path),
+// the rest build the S2D pixel rows, one warp per row.  Each thread emits two
+// neighbouring S2D pixels from 32-bit loads: the 12 input bytes of a pixel
+// pair start 4-byte aligned in row 2*h4 (Hp, Wp even) and 2 bytes off in row
+// 2*h4+1 when Wp % 4 == 2 (funnel-shifted from the aligned words around
+// them); 7 loads per 2 pixels instead of 12 16-bit ones.  The last pixel
+// (pair) of a row keeps the 16-bit loads (no read past the row's end).
+__device__ __forceinline__ uint4 s2d_pixel16(const uint16_t* r0, const uint16_t* r1, int w4) {
+  const uint32_t a0 = __ldg(r0 + 3 * w4), a1 = __ldg(r0 + 3 * w4 + 1), a2 = __ldg(r0 + 3 * w4 + 2);
+  const uint32_t b0 = __ldg(r1 + 3 * w4), b1 = __ldg(r1 + 3 * w4 + 1), b2 = __ldg(r1 + 3 * w4 + 2);
+  return make_uint4(a0 | (a1 << 16), a2 | (b0 << 16), b1 | (b2 << 16), 0u);
+}
+template <typename T>
+__device__ __forceinline__ void s2d_weight_elems(const T* __restrict__ w, T* __restrict__ w4, int K, int R, int S,
+                                                 int C, int64_t wsk, int64_t wst, int R4, int S4, int64_t first,
+                                                 int64_t step) {
+  const int64_t total = (int64_t)K * R4 * S4 * 16;
+  for (int64_t i = first; i < total; i += step) {
+    const int ch = (int)(i % 16);
+    int64_t t = i / 16;
+    const int j = (int)(t % S4);
+    t /= S4;
+    const int ii = (int)(t % R4);
+    const int k = (int)(t / R4);
+    T v = 0;
+    if (ch < 4 * C) {
+      const int ab = ch / C, c = ch - ab * C;
+      const int r = 2 * ii + ab / 2, s = 2 * j + ab % 2;
+      if (r < R && s < S) v = w[k * wsk + (int64_t)(r * S + s) * wst + c];
+    }
+    w4[i] = v;
+  }
+}
+__global__ void s2d_stem_c3_kernel(const uint8_t* __restrict__ x, uint4* __restrict__ x4, int Hp, int Wp, int Hp4,
+                                   int Wp4, int rows, int row_blocks, const uint8_t* __restrict__ w,
+                                   uint8_t* __restrict__ w4, int K, int R, int S, int64_t wsk, int64_t wst, int R4,
+                                   int S4) {
+  const int wblocks = gridDim.x - row_blocks;  // the first blocks: they run in the first wave, not the tail
+  if ((int)blockIdx.x < wblocks) {
+    s2d_weight_elems<uint8_t>(w, w4, K, R, S, 3, wsk, wst, R4, S4, (int64_t)blockIdx.x * blockDim.x + threadIdx.x,
+                              (int64_t)wblocks * blockDim.x);
+    return;
+  }
+  const int rb = blockIdx.x - wblocks;
+  const bool odd1 = (Wp * 3) % 4 != 0;  // row 2*h4+1 starts 2 bytes past a 4-byte boundary
+  const int pairs = Wp4 / 2 - 1;        // pairs with whole-word loads (the last pair / pixel is 16-bit)
+  // one warp per S2D row (a row has ~Wp/4 pairs: a whole block per row left
+  // most of its threads idle)
+  const int wpb = blockDim.x / 32, lane = threadIdx.x & 31;
+  for (int row = rb * wpb + threadIdx.x / 32; row < rows; row += row_blocks * wpb) {
+    const int n = row / Hp4, h4 = row - n * Hp4;
+    const uint8_t* r0b = x + ((int64_t)n * Hp + 2 * h4) * Wp * 3;
+    const uint8_t* r1b = r0b + Wp * 3;
+    const uint32_t* r0 = reinterpret_cast<const uint32_t*>(r0b);
+    const uint32_t* r1 = reinterpret_cast<const uint32_t*>(r1b - (odd1 ? 2 : 0));
+    uint4* dst = x4 + (int64_t)row * Wp4;
+    for (int j = lane; j < pairs; j += 32) {
+      const uint32_t a0 = __ldg(r0 + 3 * j), a1 = __ldg(r0 + 3 * j + 1), a2 = __ldg(r0 + 3 * j + 2);
+      uint32_t b0, b1, b2;
+      if (odd1) {
+        const uint32_t m0 = __ldg(r1 + 3 * j), m1 = __ldg(r1 + 3 * j + 1), m2 = __ldg(r1 + 3 * j + 2),
+                       m3 = __ldg(r1 + 3 * j + 3);
+        b0 = __funnelshift_r(m0, m1, 16);
+        b1 = __funnelshift_r(m1, m2, 16);
+        b2 = __funnelshift_r(m2, m3, 16);
+      } else {
+        b0 = __ldg(r1 + 3 * j);
+        b1 = __ldg(r1 + 3 * j + 1);
+        b2 = __ldg(r1 + 3 * j + 2);
+      }
+      dst[2 * j] = make_uint4(a0, (a1 & 0xFFFFu) | (b0 << 16), (b0 >> 16) | (b1 << 16), 0u);
+      dst[2 * j + 1] = make_uint4((a1 >> 16) | (a2 << 16), (a2 >> 16) | (b1 & 0xFFFF0000u), b2, 0u);
+    }
+    // the row's last pair / odd pixel: 16-bit loads
+    const uint16_t* h0 = reinterpret_cast<const uint16_t*>(r0b);
+    const uint16_t* h1 = reinterpret_cast<const uint16_t*>(r1b);
+    for (int w4i = 2 * pairs + lane; w4i < Wp4; w4i += 32) dst[w4i] = s2d_pixel16(h0, h1, w4i);
+  }
+}
+
 // fp16 C = 3 stem: 32-byte S2D pixels (halfs (a*2+b)*3+c, 4 zero halfs);
 // the input pixel pair (2*w4, 2*w4+1) of a row is 12 contiguous bytes at a
 // 4-byte aligned offset (Wp even): three 32-bit loads per row.
@@ -320,6 +402,23 @@ Status s2d_stem(const Problem& pb, const void* x, const void* w, void* x4, void*
     const int rows = pb.n * hp4;
     tzcdev::s2d_rows_c3_f16_kernel<<<std::min(rows, 148 * 16), 128, 0, st>>>((const uint8_t*)x, (uint4*)x4, pb.hp,
                                                                              pb.wp, hp4, wp4, rows);
+  } else if (pb.c == 3 && pb.hp % 2 == 0 && pb.wp % 2 == 0 && reinterpret_cast<uintptr_t>(x) % 4 == 0 && wp4 >= 2) {
+    // rows + weights in one launch (the weights' blocks run beside the rows')
+    const int rows = pb.n * hp4;
+    const int row_blocks = std::min((rows + 3) / 4, 148 * 16);  // 4 warps = 4 rows per block
+    const int64_t nw = (int64_t)pb.ngemm * r4 * s4 * 16;
+    const int wblocks = (int)std::min<int64_t>((nw + 255) / 256, 64);
+    tzcdev::s2d_stem_c3_kernel<<<row_blocks + wblocks, 128, 0, st>>>(
+        (const uint8_t*)x, (uint4*)x4, pb.hp, pb.wp, hp4, wp4, rows, row_blocks, (const uint8_t*)w, (uint8_t*)w4,
+        pb.ngemm, pb.r, pb.s, pb.w_stride_k, pb.w_stride_tap, r4, s4);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    const int64_t padded = (npix4 + 7) / 8 * 8;
+    if (padded > npix4) {
+      tzcdev::zero_tail_kernel<<<1, 32, 0, st>>>((uint4*)x4, npix4, padded);
+      g_launches.fetch_add(1, std::memory_order_relaxed);
+    }
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? Status() : Status(TZC_E_DEVICE, cudaGetErrorString(e));
   } else if (pb.c == 3 && pb.hp % 2 == 0 && pb.wp % 2 == 0 && reinterpret_cast<uintptr_t>(x) % 2 == 0) {
     const int rows = pb.n * hp4;
     tzcdev::s2d_rows_c3_kernel<<<std::min(rows, 148 * 16), 128, 0, st>>>((const uint8_t*)x, (uint4*)x4, pb.hp, pb.wp,

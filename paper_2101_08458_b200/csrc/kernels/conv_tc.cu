@@ -38,6 +38,16 @@ constexpr int kStaticSmem = 0;
 #endif
 // General-kernel SMEM: EG int8 staging tiles (128 x BN) + the A/B ring + barriers.
 int ring_smem(int bn, int kb, int eg, int stages) { return 1024 + eg * 128 * bn + stages * (128 + bn) * kb + 256; }
+// Resident-B variant: the ring carries A blocks only, B (num_kb blocks) stays.
+int bres_smem(int bn, int kb, int eg, int stages, int num_kb) {
+  return 1024 + eg * 128 * bn + stages * 128 * kb + num_kb * bn * kb + 256 + 8 * num_kb;
+}
+// A-ring depth with all of B resident (0: B does not fit next to a 4-deep ring).
+int bres_stages(int bn, int kb, int eg, int num_kb, int static_smem) {
+  const int avail = 227 * 1024 - static_smem - 1024 - 256 - 8 * num_kb - eg * 128 * bn - num_kb * bn * kb;
+  const int st = std::min(8, avail / (128 * kb));
+  return st >= 4 ? st : 0;
+}
 using tzcb200::Options;
 // Ping-pong epilogue groups for tiles of <= o.pingpong_kb K blocks.
 int epi_groups_for(int kb_per_tile, const Options& o) { return kb_per_tile <= o.pingpong_kb ? 2 : 1; }
@@ -244,7 +254,8 @@ Status launch_kernel(const ConvKernelParams& p, int grid, cudaStream_t stream) {
   static std::atomic<uint64_t> attr_done{0};  // per instantiation, one bit per device
   Status sa = ensure_smem_attr(kern, attr_done);
   if (!sa.ok()) return sa;
-  const int smem = ring_smem(BN, KB, p.tma_store ? p.epi_groups : 0, p.stages);  // staging only for TMA stores
+  const int eg = p.tma_store ? p.epi_groups : 0;  // staging only for TMA stores
+  const int smem = p.b_res ? bres_smem(BN, KB, eg, p.stages, p.num_kb) : ring_smem(BN, KB, eg, p.stages);
   cudaError_t e = launch_pdl(kern, dim3(grid), dim3(tzcdev::EpiCfg<BN>::THREADS), smem, stream, p);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   note_launch(0, 1, 128, BN, KB, AM, grid, p.splits);
@@ -538,6 +549,13 @@ Status plan_problem(const Problem& pb_in, const Options& o, tzc_plan* plan) {
   plan->grid = std::min(wsplit.full + (tiles - wsplit.full) * splits, sms);
   plan->smem_bytes = ring_smem(bn, kb, eg, plan->stages);
   plan->workspace_bytes = splits > 1 ? (int64_t)splits * (M - red_m0) * pb.ngemm * 4 : 0;
+  if (o.b_res && splits == 1 && wsplit.full == tiles && plan->grid % tiles_n == 0 && tiles >= 2 * plan->grid) {
+    const int st = bres_stages(bn, kb, 0, num_kb, kStaticSmem);  // as run_problem decides (no TMA-store staging)
+    if (st) {
+      plan->stages = st;
+      plan->smem_bytes = bres_smem(bn, kb, 0, st, num_kb);
+    }
+  }
   return Status();
 }
 
@@ -1156,6 +1174,18 @@ Status run_problem(const Problem& pb, const Options& o, const void* a, const voi
       st = workspace(3, (size_t)p.num_tiles * 16 * sizeof(int32_t), &cnt, stream);
       if (!st.ok()) return st;
       p.splitk_cnt = static_cast<int32_t*>(cnt);
+    }
+  }
+  // Weight-stationary CTAs ("b_res"): when every unit of a CTA has the same
+  // N tile (grid a multiple of tiles_n) and the whole B tile fits beside a
+  // >= 4-deep A ring, B is loaded once per CTA instead of once per tile.
+  p.b_res = 0;
+  if (o.b_res && plan.splits == 1 && p.full_units == p.num_tiles && plan.grid % plan.tiles_n == 0 &&
+      p.num_tiles >= 2 * plan.grid) {
+    const int st = bres_stages(plan.bn, plan.bk_bytes, p.tma_store ? p.epi_groups : 0, p.num_kb, kStaticSmem);
+    if (st) {
+      p.b_res = 1;
+      p.stages = st;
     }
   }
   const Entry* ent = find_entry(plan.bn, plan.bk_bytes, pb.f16, pb.a_mode, pb.b_kn);

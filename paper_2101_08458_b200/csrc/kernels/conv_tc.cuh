@@ -128,6 +128,7 @@ struct alignas(64) ConvKernelParams {
   int32_t mt;                  // shifted-window: 128-row tiles per work unit
   int32_t nacc;                // shifted-window: TMEM accumulators in flight (2 or 4)
   int32_t stages;              // general kernel: SMEM ring depth
+  int32_t b_res;               // general kernel: the CTA's whole B tile (all K blocks) stays in SMEM; the ring streams A only
   // work split: units [0, full_units) are whole tiles; the remaining tiles
   // are split `splits` ways along K, their int32 partials stored at rows
   // [red_m0, red_m0 + red_rows) of the workspace and combined by the fix-up
@@ -604,11 +605,14 @@ __global__ void __launch_bounds__(EpiCfg<BN>::THREADS, 1) conv_tc_kernel(const _
   uint8_t* sStage = smem;  // TMA-store staging: EG tiles of STAGING_BYTES (1024-aligned)
   uint8_t* sA = smem + (p.tma_store ? EG * Cfg::STAGING_BYTES : 0);
   uint8_t* sB = sA + STAGES * Cfg::A_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * Cfg::B_BYTES);
+  // b_res: sB holds all num_kb K blocks of B (loaded once per CTA: every unit
+  // of a CTA has the same N tile, host-checked), else one B block per stage
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + (p.b_res ? p.num_kb : STAGES) * Cfg::B_BYTES);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* bfull = tempty + 2;  // b_res: one barrier per resident B block
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bfull + (p.b_res ? p.num_kb : 1));
 
   const uint32_t warp = warp_id();
   const uint32_t lane = threadIdx.x & 31;
@@ -627,6 +631,8 @@ __global__ void __launch_bounds__(EpiCfg<BN>::THREADS, 1) conv_tc_kernel(const _
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], 16 / EG);  // the warps that drain buffer a
     }
+    if (p.b_res)
+      for (int kb = 0; kb < p.num_kb; ++kb) mbar_init(&bfull[kb], 1);
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc<Cfg::TMEM_COLS>(tmem_slot);
@@ -652,6 +658,26 @@ __global__ void __launch_bounds__(EpiCfg<BN>::THREADS, 1) conv_tc_kernel(const _
       uint32_t g = 0;  // K blocks seen (both producers walk every block, act on their parity)
       int stage = 0;
       uint32_t phase = 0;
+      if (p.b_res && (int)blockIdx.x < num_units) {
+        // the CTA's B tile, every K block once (units u = blockIdx.x + j * grid
+        // with grid % tiles_n == 0 share n_tile = blockIdx.x % tiles_n); one
+        // barrier per block so the first tile's MMAs start on block 0; the two
+        // producers split the blocks like the ring
+        const int n0 = (int)(blockIdx.x - fdiv(blockIdx.x, p.fd_tiles_n) * p.tiles_n) * BN;
+        for (int kb = (int)pj; kb < p.num_kb; kb += 2) {
+          const int tap = (int)fdiv(kb, p.fd_cblocks);
+          const int cb = kb - tap * p.c_blocks;
+          uint8_t* dB = sB + kb * Cfg::B_BYTES;
+          mbar_expect_tx(&bfull[kb], (uint32_t)Cfg::B_BYTES);
+          if constexpr (kBMN) {
+#pragma unroll
+            for (int j = 0; j < BN / 64; ++j)
+              tma_load_2d_p(dB + j * (KE * 128), &p.tmB, &bfull[kb], n0 + 64 * j, kb * KE, p.pol_b);
+          } else {
+            tma_load_3d_p(dB, &p.tmB, &bfull[kb], cb * KE, n0, tap, p.pol_b);
+          }
+        }
+      }
       for (int u = blockIdx.x, it = 0; u < num_units; u += gridDim.x, ++it) {
         int tile, split, kb0, kb1;
         unit_decode(p, u, tile, split, kb0, kb1);
@@ -678,7 +704,7 @@ __global__ void __launch_bounds__(EpiCfg<BN>::THREADS, 1) conv_tc_kernel(const _
           const int cb = kb - tap * p.c_blocks;
           uint8_t* dA = sA + stage * Cfg::A_BYTES;
           uint8_t* dB = sB + stage * Cfg::B_BYTES;
-          mbar_expect_tx(&full[stage], Cfg::STAGE_BYTES);
+          mbar_expect_tx(&full[stage], p.b_res ? Cfg::A_BYTES : Cfg::STAGE_BYTES);
           if constexpr (kAMode == A_IM2COL) {
             const int r = (int)fdiv(tap, p.fd_s), s = tap - r * p.S;
             tma_load_im2col_4d(dA, &p.tmA, &full[stage], cb * KE, ow * p.stride, oh * p.stride, img,
@@ -686,12 +712,14 @@ __global__ void __launch_bounds__(EpiCfg<BN>::THREADS, 1) conv_tc_kernel(const _
           } else {
             tma_load_2d_p(dA, &p.tmA, &full[stage], kb * KE, m0, p.pol_a);
           }
-          if constexpr (kBMN) {
+          if (!p.b_res) {
+            if constexpr (kBMN) {
 #pragma unroll
-            for (int j = 0; j < BN / 64; ++j)
-              tma_load_2d_p(dB + j * (KE * 128), &p.tmB, &full[stage], n0 + 64 * j, kb * KE, p.pol_b);
-          } else {
-            tma_load_3d_p(dB, &p.tmB, &full[stage], cb * KE, n0, tap, p.pol_b);
+              for (int j = 0; j < BN / 64; ++j)
+                tma_load_2d_p(dB + j * (KE * 128), &p.tmB, &full[stage], n0 + 64 * j, kb * KE, p.pol_b);
+            } else {
+              tma_load_3d_p(dB, &p.tmB, &full[stage], cb * KE, n0, tap, p.pol_b);
+            }
           }
           if (++stage == STAGES) {
             stage = 0;
@@ -717,11 +745,12 @@ __global__ void __launch_bounds__(EpiCfg<BN>::THREADS, 1) conv_tc_kernel(const _
       if (lane == 0 && it < 10) TZC_TRACE_POINT(11 + 5 * it);
       for (int kb = kb0; kb < kb1; ++kb) {
         mbar_wait(&full[stage], phase);
+        if (p.b_res && it == 0) mbar_wait(&bfull[kb], 0);
         tc_fence_after();
         if (lane == 0 && kb == kb0 && it < 10) TZC_TRACE_POINT(12 + 5 * it);
         {  // whole warp, warp-uniform descriptors: UTCIMMA from uniform registers
           const uint32_t a_base = smem_u32(sA + stage * Cfg::A_BYTES);
-          const uint32_t b_base = smem_u32(sB + stage * Cfg::B_BYTES);
+          const uint32_t b_base = smem_u32(sB + (p.b_res ? kb : stage) * Cfg::B_BYTES);
 #pragma unroll
           for (int k = 0; k < MMAS; ++k) {
             const uint64_t adesc = smem_desc_kmajor(a_base + 32 * k, KB);

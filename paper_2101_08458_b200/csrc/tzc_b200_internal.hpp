@@ -63,6 +63,7 @@ struct Options {
   int st256 = 1;                // 256-bit epilogue stores where aligned
   int l2_hints = 1;             // 1: A loads evict-first; 2: B loads evict-last
   int tma_store = 0;            // int8 TMA-store epilogue: 0 never, 1 always, 2 by K
+  int b_res = 0;                // general kernel: keep the CTA's whole B tile in SMEM when it fits
   int stem_fused = 0;           // C = 3 stride-2 int8 stem: space-to-depth fused into the kernel (stem_ws.cuh;
                                 // correct, but slower than the separate S2D pass: DESIGN.md §8 finding 10)
 };

@@ -124,3 +124,18 @@ def test_s2d_stem_f16(cuda, n, hp, k):
     o = (hp - 7) // 2 + 1
     s0 = Orc.random_tensor("fp32", (n, o, o, k), 342)
     assert rel_dev(Orc.conv2d_nhwc(x, w, 2, s0, fp16=True), run(cuda, x, w, 2, s0, epilogue="f32")) <= 1e-3
+
+
+@pytest.mark.parametrize("n,hp,wp", [(2, 228, 228), (3, 64, 60), (2, 30, 36), (4, 12, 8), (1, 10, 14), (2, 22, 18)])
+def test_s2d_stem_row_widths(cuda, n, hp, wp):
+    """The one-launch S2D (rows from 32-bit loads + the weight rearrangement):
+    Wp % 4 == 0 (row 2*h4+1 word-aligned) and == 2 (funnel-shifted), an even
+    and an odd number of S2D pixels per row (the last pixel / pair on 16-bit
+    loads), rectangular images; int32 and fused requant bit-exact."""
+    x = Orc.random_tensor("u8", (n, hp, wp, 3), 320 + wp)
+    w = Orc.random_tensor("i8", (64, 7, 7, 3), 321)
+    ref = Orc.conv2d_nhwc(x, w, 2)
+    xd, wd = to_dev(x, cuda), to_dev(w, cuda)
+    assert np.array_equal(D.conv2d(xd, wd, 2).cpu().numpy(), ref)
+    q = D.conv2d(xd, wd, 2, epilogue="requant_i8", scale=2.0 ** -10).cpu().numpy()
+    assert np.array_equal(q, Orc.requant_i8(ref, 2.0 ** -10))
