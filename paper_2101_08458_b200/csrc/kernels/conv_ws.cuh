@@ -176,14 +176,24 @@ __global__ void __launch_bounds__(EpiCfg<BN>::THREADS, 1) conv_ws_kernel(const _
                   if (elect_one()) umma<kF16>(tmem_d, at + pa[i], b0 + pb[i], IDESC, i > 0 ? 1u : 0u);
               }
             }
-          } else {
-            for (int t = 0; t < MT; ++t) {
-              // tile t of the unit: A rows shifted by t*128 (16-byte descriptor units)
-              const uint64_t at = a0 + (uint64_t)(t * 8 * KB);
-              const uint32_t tmem_d = tmem_acc + t * BN;
+          } else if (MT == 1) {
 #pragma unroll 2
-              for (int i = 0; i < n_mma; ++i)
-                if (elect_one()) umma<kF16>(tmem_d, at + p.mma_a[i], b0 + p.mma_b[i], IDESC, (cb > 0 || i > 0) ? 1u : 0u);
+            for (int i = 0; i < n_mma; ++i)
+              if (elect_one()) umma<kF16>(tmem_acc, a0 + p.mma_a[i], b0 + p.mma_b[i], IDESC, (cb > 0 || i > 0) ? 1u : 0u);
+          } else {
+            // (tap, K step) outer, tile t of the unit inner: each offset pair
+            // is read from the parameter bank once per MT MMAs (t-outer paid
+            // two constant loads per MMA on the issue path: 69 cycles per N=64
+            // MMA against the 48-cycle SMEM bound).  Each accumulator still
+            // receives its MMAs in order i = 0, 1, ... (identical sums).
+#pragma unroll 1
+            for (int i = 0; i < n_mma; ++i) {
+              const uint64_t ai = a0 + p.mma_a[i];
+              const uint64_t bi = b0 + p.mma_b[i];
+              const uint32_t accum = (cb > 0 || i > 0) ? 1u : 0u;
+#pragma unroll
+              for (int t = 0; t < 4; ++t)  // tile t: A rows shifted by t*128 (16-byte descriptor units)
+                if (t < MT && elect_one()) umma<kF16>(tmem_acc + t * BN, ai + (uint64_t)(t * 8 * KB), bi, IDESC, accum);
             }
           }
           if (elect_one()) {
