@@ -396,13 +396,14 @@ __global__ void s2d_weight_kernel(const T* __restrict__ w, T* __restrict__ w4, i
 namespace tzcb200 {
 
 Status s2d_stem(const Problem& pb, const void* x, const void* w, void* x4, void* w4, int hp4, int wp4, int r4, int s4,
-                cudaStream_t st) {
+                cudaStream_t st, bool one_launch) {
   const int64_t npix4 = (int64_t)pb.n * hp4 * wp4;
   if (pb.f16) {  // C = 3, even extents (s2d_eligible)
     const int rows = pb.n * hp4;
     tzcdev::s2d_rows_c3_f16_kernel<<<std::min(rows, 148 * 16), 128, 0, st>>>((const uint8_t*)x, (uint4*)x4, pb.hp,
                                                                              pb.wp, hp4, wp4, rows);
-  } else if (pb.c == 3 && pb.hp % 2 == 0 && pb.wp % 2 == 0 && reinterpret_cast<uintptr_t>(x) % 4 == 0 && wp4 >= 2) {
+  } else if (one_launch && pb.c == 3 && pb.hp % 2 == 0 && pb.wp % 2 == 0 && reinterpret_cast<uintptr_t>(x) % 4 == 0 &&
+             wp4 >= 2) {
     // rows + weights in one launch (the weights' blocks run beside the rows')
     const int rows = pb.n * hp4;
     const int row_blocks = std::min((rows + 3) / 4, 148 * 16);  // 4 warps = 4 rows per block

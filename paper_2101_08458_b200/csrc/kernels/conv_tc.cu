@@ -1007,7 +1007,7 @@ Status run_problem(const Problem& pb, const Options& o, const void* a, const voi
       const int eb = pb.f16 ? 2 : 1;
       st = workspace(1, (size_t)(((int64_t)q.n * q.hp * q.wp + 7) / 8 * 8) * 16 * eb, &x4, stream);
       if (st.ok()) st = workspace(2, (size_t)q.ngemm * q.taps * 16 * eb, &w4, stream);
-      if (st.ok()) st = s2d_stem(pb, a, b, x4, w4, q.hp, q.wp, q.r, q.s, stream);
+      if (st.ok()) st = s2d_stem(pb, a, b, x4, w4, q.hp, q.wp, q.r, q.s, stream, o.s2d_one != 0);
       if (st.ok()) st = run_ws(q, w, o, x4, w4, seed, out, ep, stream);
       return st;
     }
@@ -1142,7 +1142,7 @@ Status run_problem(const Problem& pb, const Options& o, const void* a, const voi
   // without the TMA-store staging tiles the ring gets their SMEM
   if (!p.tma_store) p.stages = ring_stages(plan.bn, plan.bk_bytes, 0);
   if (o.pair && ep.kind == tzcdev::EP_REQUANT_I8 && p.vec_ok && pb.ngemm % plan.bn == 0 && !pb.f16 && !pb.b_kn &&
-      plan.splits == 1 && p.full_units == p.num_tiles && p.num_kb >= o.pair_min_kb &&
+      plan.splits == 1 && p.full_units == p.num_tiles && p.num_kb >= o.pair_min_kb && plan.bn >= o.pair_bn &&
       p.epi_groups == 1 && plan.bk_bytes == 128 && (plan.bn == 128 || plan.bn == 256) &&
       (pb.a_mode == tzcdev::A_TILED || pb.a_mode == tzcdev::A_IM2COL) && num_sms() >= 2) {
     // CTA pairs: 256-row tiles, each CTA loads its A rows and half the B rows

@@ -58,8 +58,16 @@ struct Options {
   int ws_1x1 = 0;               // ... for every 1x1 stride-1 conv
   int bn = 0;                   // force the N tile (0 = automatic)
   int tma_store_k = 64;         // tma_store == 2: TMA-store epilogue for GEMM K <= this many bytes
-  int pair_min_kb = 16;         // CTA pairs for layers with >= this many K blocks
-  int pair = 0;                 // CTA-pair (cta_group::2) kernel for eligible int8 layers
+  // CTA-pair (cta_group::2) kernel for eligible int8 requant layers with >=
+  // pair_min_kb K blocks and N tiles >= pair_bn: each CTA loads half of B, so
+  // operand bytes per MMA drop 12 -> 8 KB at BN = 256 (the general kernel is
+  // bound by the ~60 B/clk/SM L2->SMEM operand stream; tools/tma_probe.cu).
+  // Measured with two producer warps: 4-9% faster for BN = 256 layers with
+  // >= 8 K blocks, slower for BN = 128 and for 4-block layers.
+  int pair_min_kb = 8;
+  int pair = 1;
+  int pair_bn = 256;
+  int s2d_one = 1;              // int8 C=3 stem: S2D rows + weight rearrangement in one launch
   int st256 = 1;                // 256-bit epilogue stores where aligned
   int l2_hints = 1;             // 1: A loads evict-first; 2: B loads evict-last
   int tma_store = 0;            // int8 TMA-store epilogue: 0 never, 1 always, 2 by K
@@ -101,7 +109,7 @@ Status im2col_pad(const Problem& pb, const void* x, void* a, int kp, cudaStream_
 Status weight_pad(const Problem& pb, const void* w, void* b, int kp, cudaStream_t st);
 
 Status s2d_stem(const Problem& pb, const void* x, const void* w, void* x4, void* w4, int hp4, int wp4, int r4, int s4,
-                cudaStream_t st);
+                cudaStream_t st, bool one_launch = true);
 
 extern std::atomic<uint64_t> g_launches;
 // the calling thread's most recent launch (tzc_b200_last_launch)

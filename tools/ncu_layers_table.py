@@ -16,7 +16,8 @@ def main(csv_path, log_path):
         e = per.setdefault(key, {"kernel": r["Kernel Name"].split("(")[0].replace("void ", "").strip()})
         v = float(r["Metric Value"].replace(",", ""))
         u = r["Metric Unit"]
-        scale = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0,
+        scale = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3,
+                 "byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0,
                  "Gbyte": 1e3, "%": 1.0}.get(u, 1.0)
         e[r["Metric Name"]] = v * scale
     L = list(per.values())

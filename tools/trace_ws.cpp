@@ -6,6 +6,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <algorithm>
+#include <string>
 #include <vector>
 
 #include "tzc_b200.h"
@@ -33,6 +34,18 @@ int main(int argc, char** argv) {
   tzc_epilogue ep{TZC_EP_REQUANT_I8, 1.0f / 4096};
   if (argc > 7) tzc_debug_flags(atoi(argv[7]));
   if (argc > 8) tzc_b200_set_option("shifted_window", atoi(argv[8]));
+  if (const char* env = getenv("TZC_OPTS")) {  // "name=value,name=value"
+    std::string s(env);
+    size_t i = 0;
+    while (i < s.size()) {
+      size_t j = s.find(',', i);
+      if (j == std::string::npos) j = s.size();
+      const std::string kv = s.substr(i, j - i);
+      const size_t eq = kv.find('=');
+      if (eq != std::string::npos) tzc_b200_set_option(kv.substr(0, eq).c_str(), atoi(kv.substr(eq + 1).c_str()));
+      i = j + 1;
+    }
+  }
   // warm the clocks first: a few hundred launches (~50-100 ms) so the traced
   // launches run at the sustained SM clock, not the idle one (a trace taken
   // right after start-up ran at ~1 GHz)
