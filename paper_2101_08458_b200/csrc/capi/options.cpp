@@ -49,6 +49,7 @@ const Knob kKnobs[] = {
     {"pair_min_kb", &Options::pair_min_kb, 0, 1 << 20, nullptr},
     {"pair_bn", &Options::pair_bn, 0, 256, nullptr},
     {"s2d_one", &Options::s2d_one, 0, 1, nullptr},
+    {"producers", &Options::producers, 1, 2, nullptr},
     {"pair", &Options::pair, 0, 1, nullptr},
     {"st256", &Options::st256, 0, 1, nullptr},
     {"l2_hints", &Options::l2_hints, 0, 3, nullptr},

@@ -1043,6 +1043,7 @@ Status run_problem(const Problem& pb, const Options& o, const void* a, const voi
 #endif
   p.pol_a = (o.l2_hints & 1) ? tzcdev::kL2EvictFirst : 0;
   p.pol_b = (o.l2_hints & 2) ? tzcdev::kL2EvictLast : 0;
+  p.producers = o.producers;
   // ---- A operand
   if (pb.a_mode == tzcdev::A_TILED) {
     cuuint64_t dims[2] = {(cuuint64_t)pb.a_kdim, (cuuint64_t)pb.a_rows};

@@ -129,6 +129,7 @@ struct alignas(64) ConvKernelParams {
   int32_t nacc;                // shifted-window: TMEM accumulators in flight (2 or 4)
   int32_t stages;              // general kernel: SMEM ring depth
   int32_t b_res;               // general kernel: the CTA's whole B tile (all K blocks) stays in SMEM; the ring streams A only
+  int32_t producers;           // general / pair kernel: TMA producer warps (1: warp 0; 2: warps 0 and 3, alternate K blocks)
   // work split: units [0, full_units) are whole tiles; the remaining tiles
   // are split `splits` ways along K, their int32 partials stored at rows
   // [red_m0, red_m0 + red_rows) of the workspace and combined by the fix-up
@@ -647,7 +648,7 @@ __global__ void __launch_bounds__(EpiCfg<BN>::THREADS, 1) conv_tc_kernel(const _
 
   const int num_units = p.full_units + (p.num_tiles - p.full_units) * p.splits;
 
-  if (warp == 0 || warp == 3) {
+  if (warp == 0 || (warp == 3 && p.producers == 2)) {
     // ===================== TMA producers =====================
     // Two producer warps take alternate K blocks (tools/tma_probe.cu: one
     // issuing thread that waits on its ring between loads completes tiled TMA
@@ -655,6 +656,7 @@ __global__ void __launch_bounds__(EpiCfg<BN>::THREADS, 1) conv_tc_kernel(const _
     // several warps overlap, ~60 B/clk/SM from L2).
     if (lane == 0) {
       const uint32_t pj = warp == 0 ? 0u : 1u;
+      const uint32_t np = p.producers == 2 ? 2u : 1u;
       uint32_t g = 0;  // K blocks seen (both producers walk every block, act on their parity)
       int stage = 0;
       uint32_t phase = 0;
@@ -664,7 +666,7 @@ __global__ void __launch_bounds__(EpiCfg<BN>::THREADS, 1) conv_tc_kernel(const _
         // barrier per block so the first tile's MMAs start on block 0; the two
         // producers split the blocks like the ring
         const int n0 = (int)(blockIdx.x - fdiv(blockIdx.x, p.fd_tiles_n) * p.tiles_n) * BN;
-        for (int kb = (int)pj; kb < p.num_kb; kb += 2) {
+        for (int kb = (int)pj; kb < p.num_kb; kb += (int)np) {
           const int tap = (int)fdiv(kb, p.fd_cblocks);
           const int cb = kb - tap * p.c_blocks;
           uint8_t* dB = sB + kb * Cfg::B_BYTES;
@@ -691,7 +693,7 @@ __global__ void __launch_bounds__(EpiCfg<BN>::THREADS, 1) conv_tc_kernel(const _
           ow = rem - oh * p.OW;
         }
         for (int kb = kb0; kb < kb1; ++kb, ++g) {
-          if ((g & 1u) != pj) {
+          if (np == 2 && (g & 1u) != pj) {
             if (++stage == STAGES) {
               stage = 0;
               phase ^= 1;

@@ -83,11 +83,12 @@ __global__ void __launch_bounds__(EpiCfg<BN>::THREADS, 1) conv_tc2_kernel(const 
 
   const int num_units = p.num_tiles;  // pair tiles
 
-  if (warp == 0 || warp == 3) {
+  if (warp == 0 || (warp == 3 && p.producers == 2)) {
     // two producer warps, alternate K blocks (as conv_tc_kernel: loads issued
     // from one waiting thread complete ~serially, tools/tma_probe.cu)
     if (lane == 0) {
       const uint32_t pj = warp == 0 ? 0u : 1u;
+      const uint32_t np = p.producers == 2 ? 2u : 1u;
       uint32_t g = 0;
       const uint32_t full0 = mapa_shared(smem_u32(full), 0);  // the leader's full[0]
       int stage = 0;
@@ -103,7 +104,7 @@ __global__ void __launch_bounds__(EpiCfg<BN>::THREADS, 1) conv_tc2_kernel(const 
           ow = rem - oh * p.OW;
         }
         for (int kb = 0; kb < p.num_kb; ++kb, ++g) {
-          if ((g & 1u) != pj) {
+          if (np == 2 && (g & 1u) != pj) {
             if (++stage == STAGES) {
               stage = 0;
               phase ^= 1;

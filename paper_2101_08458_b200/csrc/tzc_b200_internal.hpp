@@ -68,6 +68,7 @@ struct Options {
   int pair = 1;
   int pair_bn = 256;
   int s2d_one = 1;              // int8 C=3 stem: S2D rows + weight rearrangement in one launch
+  int producers = 2;            // TMA producer warps of the general / pair kernels (1 or 2)
   int st256 = 1;                // 256-bit epilogue stores where aligned
   int l2_hints = 1;             // 1: A loads evict-first; 2: B loads evict-last
   int tma_store = 0;            // int8 TMA-store epilogue: 0 never, 1 always, 2 by K
