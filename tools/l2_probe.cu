@@ -14,7 +14,7 @@
 
 using namespace tzcdev;
 
-template <int MODE>
+template <int MODE, bool SPIN>
 __global__ void __launch_bounds__(32, 1) l2bw(const uint8_t* src, long long region, int ch, int slots, int iters,
                                               unsigned* sink) {
   extern __shared__ uint8_t raw[];
@@ -42,16 +42,19 @@ __global__ void __launch_bounds__(32, 1) l2bw(const uint8_t* src, long long regi
   uint32_t ph = 0;
   for (long long i = 0; i < iters; ++i) {
     const int s = (int)(i % slots);
-    mbar_wait(&bar[s], ph);
+    if (SPIN)
+      mbar_wait_spin(&bar[s], ph);
+    else
+      mbar_wait(&bar[s], ph);
     if (s == slots - 1) ph ^= 1;
     if (i + slots < iters) issue(s, i + slots);
   }
   if (sm[5] == 0x7f && sm[77] == 0x11) sink[0] = 1;
 }
 
-template <int MODE>
+template <int MODE, bool SPIN = false>
 void run(const uint8_t* src, long long region, int ch, int slots, int iters, unsigned* sink) {
-  auto k = l2bw<MODE>;
+  auto k = l2bw<MODE, SPIN>;
   const int smem = 1024 + ch * slots;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   k<<<148, 32, smem>>>(src, region, ch, slots, iters, sink);
@@ -70,7 +73,7 @@ void run(const uint8_t* src, long long region, int ch, int slots, int iters, uns
     if (ms < best) best = ms;
   }
   const double bytes = 148.0 * ch * iters;
-  printf("mode %d region %6.1f MB chunk %6d slots %2d: %7.2f us  %6.0f GB/s  %5.1f B/clk/SM (@1.965GHz) err=%s\n", MODE,
+  printf("%s mode %d region %6.1f MB chunk %6d slots %2d: %7.2f us  %6.0f GB/s  %5.1f B/clk/SM (@1.965GHz) err=%s\n", SPIN ? "spin" : "wait", MODE,
          region / 1e6, ch, slots, best * 1e3, bytes / (best * 1e-3) / 1e9, bytes / 148 / (best * 1e-3) / 1.965e9,
          cudaGetErrorString(cudaGetLastError()));
 }
@@ -82,14 +85,13 @@ int main() {
   cudaMalloc(&src, big);
   cudaMemset(src, 1, big);
   cudaMalloc(&sink, 64);
-  for (int ch : {8192, 16384, 32768}) {
-    for (int slots : {4, 6}) {
+  for (int ch : {8192, 16384, 32768, 65536}) {
+    for (int slots : {2, 3}) {
       if (ch * slots > 200 * 1024) continue;
       const int iters = (int)((8ll << 20) / ch);  // 8 MB per CTA
-      run<0>(src, 32ll << 20, ch, slots, iters, sink);    // 32 MB: L2 resident
-      run<1>(src, 256 * 1024, ch, slots, iters, sink);    // one 256 KB weight block, all CTAs in lockstep
-      run<2>(src, 256 * 1024, ch, slots, iters, sink);    // same, rotated start
-      run<0>(src, 1ll << 30, ch, slots, iters, sink);     // 1 GB: HBM
+      run<0, false>(src, 32ll << 20, ch, slots, iters, sink);
+      run<0, true>(src, 32ll << 20, ch, slots, iters, sink);
+      run<0, true>(src, 1ll << 30, ch, slots, iters, sink);
     }
   }
   return 0;
