@@ -151,7 +151,7 @@ TZC_API int tzc_b200_plan_conv(const tzc_conv_desc* d, tzc_plan* plan);
  * executed tile, not a plan query): kernel 0 = general (TMA tiled / im2col),
  * 1 = shifted-window, 2 = space-to-depth stem (shifted-window, pair mode),
  * 3 = CTA pair (cta_group::2, M = 256 rows per MMA), 4 = K7 GEMM (thin
- * channels).  Returns TZC_E_SHAPE if this thread has launched nothing. */
+ * channels), 5 = the stem with space-to-depth fused into the kernel.  Returns TZC_E_SHAPE if this thread has launched nothing. */
 typedef struct tzc_launch_info {
   int32_t kernel;
   int32_t cta_group;       /* 1 or 2 */

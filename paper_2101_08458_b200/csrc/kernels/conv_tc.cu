@@ -814,7 +814,7 @@ Status launch_stem(const ConvKernelParams& p, int grid, int smem, cudaStream_t s
   if (!sa.ok()) return sa;
   cudaError_t e = launch_pdl(kern, dim3(grid), dim3(tzcdev::EpiCfg<BN>::THREADS), smem, stream, p);
   g_launches.fetch_add(1, std::memory_order_relaxed);
-  note_launch(2, 1, 128 * p.mt, BN, 16, 3, grid, 1);
+  note_launch(5, 1, 128 * p.mt, BN, 16, 3, grid, 1);
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) return Status(TZC_E_DEVICE, std::string("stem_ws launch: ") + cudaGetErrorString(e));
   return Status();

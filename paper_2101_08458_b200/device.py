@@ -190,7 +190,7 @@ def launch_count() -> int:
     return int(lib().tzc_b200_launch_count())
 
 
-LAUNCH_KERNELS = {0: "general", 1: "shifted_window", 2: "s2d_stem", 3: "cta_pair", 4: "k7_gemm"}
+LAUNCH_KERNELS = {0: "general", 1: "shifted_window", 2: "s2d_stem", 3: "cta_pair", 4: "k7_gemm", 5: "stem_fused"}
 
 
 def last_launch() -> dict:

@@ -114,3 +114,30 @@ def test_split_f16(cuda):
     finally:
         D.set_splits(0)
     assert rel_dev(Orc.matmul(A, B, fp16=True), got) <= 1e-3
+
+
+@pytest.mark.parametrize("opts,n,hp", [({"b_res": 1}, 4, 100), ({"producers": 1}, 2, 20),
+                                       ({"b_res": 1, "producers": 1}, 4, 100)])
+def test_general_kernel_pipeline_options(cuda, opts, n, hp):
+    """The general kernel's operand-pipeline variants (resident B tile loaded
+    once per CTA; one or two TMA producer warps) plan the same tiles and stay
+    bit-exact, int32 and fused requant."""
+    from paper_2101_08458_b200 import device as D
+    c, k, r = 128, 128, 3
+    x = Orc.random_tensor("u8", (n, hp, hp, c), 540)
+    w = Orc.random_tensor("i8", (k, r, r, c), 541)
+    D.set_option("shifted_window", 0)
+    for kk, v in opts.items():
+        D.set_option(kk, v)
+    try:
+        xd, wd = to_dev(x, cuda), to_dev(w, cuda)
+        got = D.conv2d(xd, wd, 1).cpu().numpy()
+        assert D.last_launch()["kernel"] == "general"
+        q = D.conv2d(xd, wd, 1, epilogue="requant_i8", scale=2.0 ** -13).cpu().numpy()
+    finally:
+        D.set_option("shifted_window", 1)
+        D.set_option("b_res", 0)
+        D.set_option("producers", 2)
+    ref = Orc.conv2d_nhwc(x, w, 1)
+    assert np.array_equal(got, ref)
+    assert np.array_equal(q, Orc.requant_i8(ref, 2.0 ** -13))

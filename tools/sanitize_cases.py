@@ -38,10 +38,12 @@ def conv(n, hp, c, k, r, st, opts=(), seed=True, scale=None, label=""):
             ok = np.array_equal(got, Orc.requant_i8(Orc.conv2d_nhwc(x, w, st, s0), scale))
     finally:
         for kk, _ in opts:
-            D.set_option(kk, {"ws_mt": 0, "ws_epi_groups": 1, "splits": 0, "pair": 0, "pair_min_kb": 16,
-                              "shifted_window": 1, "tma_store": 0, "tail_split": 0, "stem_fused": 0,
-                              "splitk_inkernel": 1}[kk])
+            D.set_option(kk, {"ws_mt": 0, "ws_epi_groups": 1, "splits": 0, "pair": 1, "pair_min_kb": 8,
+                              "pair_bn": 256, "shifted_window": 1, "tma_store": 0, "tail_split": 0, "stem_fused": 0,
+                              "splitk_inkernel": 1, "b_res": 0, "producers": 2, "s2d_one": 1}[kk])  # library defaults
+    ran = D.last_launch()
     print(f"{label:34s} plan a_mode={plan['a_mode']} bm={plan['bm']} bn={plan['bn']} splits={plan['splits']} "
+          f"ran {ran['kernel']} cta_group={ran['cta_group']} bm={ran['bm']} bn={ran['bn']} "
           f"{'OK' if ok else 'MISMATCH'}", flush=True)
     return ok
 
@@ -66,6 +68,13 @@ def main():
                seed=False, scale=2.0 ** -13, label="conv_tc2 CTA pair")
     ok &= conv(2, 10, 64, 256, 1, 1, opts=[("shifted_window", 0), ("tma_store", 1)], seed=False,
                scale=2.0 ** -12, label="conv_tc TMA-store epilogue")
+    ok &= conv(3, 10, 128, 128, 3, 1, opts=[("shifted_window", 0), ("pair", 1), ("pair_min_kb", 1), ("pair_bn", 0)],
+               seed=False, scale=2.0 ** -13, label="conv_tc2 CTA pair BN128")
+    ok &= conv(4, 100, 128, 128, 3, 1, opts=[("shifted_window", 0), ("b_res", 1)], seed=False, scale=2.0 ** -13,
+               label="conv_tc resident B (301 tiles)")
+    ok &= conv(2, 10, 64, 128, 3, 1, opts=[("shifted_window", 0), ("producers", 1)], label="conv_tc one producer")
+    ok &= conv(2, 62, 3, 64, 7, 2, opts=[("s2d_one", 0)], seed=False, scale=2.0 ** -11,
+               label="s2d stem two-launch S2D")
     # fp16
     x = Orc.random_tensor("fp16", (2, 10, 10, 64), 5)
     w = Orc.random_tensor("fp16", (128, 3, 3, 64), 6)
