@@ -366,12 +366,18 @@ def run_ours(args, rank, world, local):
     rt = Cudart()
     evs = [rt.event() for _ in range(len(bufs) + 1)]
 
+    ran = {}  # layer -> the executed tile of its last eager launch (tzc_b200_last_launch)
+
     def suite(record):
         for i, b in enumerate(bufs):
             if record:
                 rt.record(evs[i], stream)
             D.conv2d(b["x"], b["w"], b["layer"].stride, epilogue=b["ep"], scale=b["scale"],
                      out=b["out"], stream=stream)
+            try:
+                ran[b["layer"].name] = D.last_launch()
+            except Exception:  # noqa: BLE001
+                pass
         if record:
             rt.record(evs[len(bufs)], stream)
 
@@ -516,7 +522,7 @@ def run_ours(args, rank, world, local):
         roof = min(spec, ops / by * pk["hbm_gbs"] / 1e3)
         layer_rows.append({"layer": L.name, "ms": ms, "tops": ops / (ms * 1e-3) / 1e12,
                            "gbs": by / (ms * 1e-3) / 1e9, "roofline_tops_spec": roof,
-                           "plan": plan_of(D, b)})
+                           "plan": plan_of(D, b), "ran": ran.get(L.name)})
     result = {
         "metric": METRIC_F16 if f16 else METRIC,
         "value": round(value, 2),

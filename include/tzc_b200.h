@@ -145,6 +145,9 @@ TZC_API int tzc_b200_gemm_i8(const tzc_gemm_desc* d, const uint8_t* a, const int
 TZC_API int tzc_b200_gemm_f16(const tzc_gemm_desc* d, const uint16_t* a, const uint16_t* b,
                       const float* c_seed, void* out, const tzc_epilogue* ep, void* stream);
 
+/* The plan a launch of this descriptor would use (descriptor only: the
+ * CTA-pair choice, which needs the fused requant epilogue, and the resident-B
+ * ring are decided at launch; tzc_b200_last_launch reports what ran). */
 TZC_API int tzc_b200_plan_conv(const tzc_conv_desc* d, tzc_plan* plan);
 
 /* What the calling thread's most recent conv/GEMM launch actually ran (the
