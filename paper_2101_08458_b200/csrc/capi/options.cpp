@@ -48,6 +48,7 @@ const Knob kKnobs[] = {
     {"tma_store_k", &Options::tma_store_k, 0, 1 << 20, nullptr},
     {"pair_min_kb", &Options::pair_min_kb, 0, 1 << 20, nullptr},
     {"pair_bn", &Options::pair_bn, 0, 256, nullptr},
+    {"pair_min_round", &Options::pair_min_round, 0, 64, nullptr},
     {"s2d_one", &Options::s2d_one, 0, 1, nullptr},
     {"producers", &Options::producers, 1, 2, nullptr},
     {"pair", &Options::pair, 0, 1, nullptr},

@@ -640,6 +640,7 @@ tzcb200::Options instruction_options(const KernelPlan& p, tzcb200::Options o) {
     o.pair = 1;
     o.pair_min_kb = 0;
     o.pair_bn = 0;
+    o.pair_min_round = 0;
     o.shifted_window = 0;
   } else {
     o.pair = 0;  // an M = 128 description is a cta_group::1 MMA

@@ -1144,6 +1144,7 @@ Status run_problem(const Problem& pb, const Options& o, const void* a, const voi
   if (!p.tma_store) p.stages = ring_stages(plan.bn, plan.bk_bytes, 0);
   if (o.pair && ep.kind == tzcdev::EP_REQUANT_I8 && p.vec_ok && pb.ngemm % plan.bn == 0 && !pb.f16 && !pb.b_kn &&
       plan.splits == 1 && p.full_units == p.num_tiles && p.num_kb >= o.pair_min_kb && plan.bn >= o.pair_bn &&
+      (int64_t)((plan.tiles_m + 1) / 2) * plan.tiles_n >= (int64_t)o.pair_min_round * (num_sms() / 2) &&
       p.epi_groups == 1 && plan.bk_bytes == 128 && (plan.bn == 128 || plan.bn == 256) &&
       (pb.a_mode == tzcdev::A_TILED || pb.a_mode == tzcdev::A_IM2COL) && num_sms() >= 2) {
     // CTA pairs: 256-row tiles, each CTA loads its A rows and half the B rows

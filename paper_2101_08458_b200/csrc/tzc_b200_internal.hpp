@@ -67,6 +67,10 @@ struct Options {
   int pair_min_kb = 8;
   int pair = 1;
   int pair_bn = 256;
+  // ... and only when the pair tiles fill >= this many rounds of SM pairs: with
+  // fewer (batch 32) a cluster's two-SM footprint backfills the SMs other graph
+  // branches leave idle worse (batch 32: 682-690 TOPS without pairs, 655-677 with)
+  int pair_min_round = 1;
   int s2d_one = 1;              // int8 C=3 stem: S2D rows + weight rearrangement in one launch
   int producers = 2;            // TMA producer warps of the general / pair kernels (1 or 2)
   int st256 = 1;                // 256-bit epilogue stores where aligned

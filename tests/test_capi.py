@@ -124,7 +124,7 @@ def test_problem_options_validation_and_candidates():
     from paper_2101_08458_b200 import device as D
     from paper_2101_08458_b200._capi import TzcError
     cands = D.tune_candidates()
-    assert cands[0] == "" and len(cands) == 17 and "bn=128" in cands
+    assert cands[0] == "" and len(cands) == 20 and "bn=128" in cands
     D.set_conv_plan((2, 10, 10, 64), (64, 3, 3, 64), 1, spec="bn=128;pingpong_kb=0")
     D.set_conv_plan((2, 10, 10, 64), (64, 3, 3, 64), 1, spec="")
     with pytest.raises(TzcError, match="unknown option"):

@@ -57,11 +57,11 @@ def test_cli_run_output_and_failing_verify(cuda, name, tmp_path):
 
 @pytest.mark.parametrize("name", ["mm_i8", "conv_nhwc_i8"])
 def test_cli_tune(cuda, name):
-    """`tzc-b200 tune`: 17 candidate plans timed on the device, the winner reported."""
+    """`tzc-b200 tune`: 20 candidate plans timed on the device, the winner reported."""
     d, args = case_args(name)
     rc, out, err = cli("tune", *args[:3], "--reps", "3")
     assert rc == 0, err
     lines = out.strip().splitlines()
     assert lines[0].startswith("plan ")
-    assert sum(ln.startswith("candidate ") for ln in lines) == 17
+    assert sum(ln.startswith("candidate ") for ln in lines) == 20
     assert lines[-1].startswith("best ")

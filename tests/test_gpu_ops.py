@@ -161,7 +161,7 @@ def test_tuner_installs_a_plan_and_results_stay_exact(cuda):
     try:
         best, log = D.tune_conv2d(x, w, 1, epilogue="requant_i8", scale=2.0 ** -12, reps=3)
         lines = log.strip().splitlines()
-        assert sum(ln.startswith("candidate ") for ln in lines) == 17 and lines[-1].startswith(f"best {best} ")
+        assert sum(ln.startswith("candidate ") for ln in lines) == 20 and lines[-1].startswith(f"best {best} ")
         assert 0 <= best < 17
         q = D.conv2d(x, w, 1, epilogue="requant_i8", scale=2.0 ** -12).cpu().numpy()
         assert np.array_equal(q, Orc.requant_i8(ref, 2.0 ** -12))

@@ -11,21 +11,28 @@ from paper_2101_08458_b200 import device as D
 from tests.gpu_helpers import to_dev
 
 pytestmark = pytest.mark.gpu
-PAIR_DEFAULT = 0  # the library defaults (conv_tc.cu g_pair, g_pair_min_kb)
-PAIR_MIN_KB = 16
+# the library defaults (tzc_b200_internal.hpp Options): pairs for BN = 256
+# layers with >= 8 K blocks whose pair tiles fill a round of SM pairs
+DEFAULTS = {"pair": 1, "pair_min_kb": 8, "pair_bn": 256, "pair_min_round": 1, "tma_store": 0, "pingpong_kb": 2}
+FORCE = {"pair_min_kb": 1, "pair_bn": 0, "pair_min_round": 0, "pingpong_kb": 0}  # (pairs need one epilogue group)
 
 
-def with_pair(on, fn):
-    """The pair kernel runs the TMA-store epilogue: force it for every tile."""
-    D.set_option("pair", on)
-    D.set_option("pair_min_kb", 1)
-    D.set_option("tma_store", 1)
+def set_opts(opts):
+    for k, v in opts.items():
+        D.set_option(k, v)
+
+
+def with_pair(on, fn, tma_store=1):
+    """Force the pair kernel (on=1) for every eligible tile, or the single-CTA
+    kernel (on=0); checks that the intended kernel ran."""
+    set_opts({"pair": on, **FORCE, "tma_store": tma_store})
     try:
-        return fn()
+        out = fn()
+        ran = D.last_launch()
+        assert ran["kernel"] == ("cta_pair" if on else "general"), ran
+        return out
     finally:
-        D.set_option("pair", PAIR_DEFAULT)
-        D.set_option("pair_min_kb", PAIR_MIN_KB)
-        D.set_option("tma_store", 0)
+        set_opts(DEFAULTS)
 
 
 @pytest.mark.parametrize("m,n,k", [(1000, 256, 512), (777, 128, 384), (4096, 256, 1024), (300, 512, 256 + 128),
@@ -67,11 +74,6 @@ def test_pair_direct_store_epilogue(cuda, m, n, k):
     a = Orc.random_tensor("u8", (m, k), 530)
     b = Orc.random_tensor("i8", (n, k), 531)
     want = Orc.requant_i8(Orc.matmul(a, b), 2.0 ** -12)
-    D.set_option("pair", 1)
-    D.set_option("pair_min_kb", 1)
-    try:
-        got = D.gemm(to_dev(a, cuda), to_dev(b, cuda), epilogue="requant_i8", scale=2.0 ** -12).cpu().numpy()
-    finally:
-        D.set_option("pair", PAIR_DEFAULT)
-        D.set_option("pair_min_kb", PAIR_MIN_KB)
+    got = with_pair(1, lambda: D.gemm(to_dev(a, cuda), to_dev(b, cuda), epilogue="requant_i8",
+                                      scale=2.0 ** -12).cpu().numpy(), tma_store=0)
     assert np.array_equal(got, want)

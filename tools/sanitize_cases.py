@@ -39,7 +39,7 @@ def conv(n, hp, c, k, r, st, opts=(), seed=True, scale=None, label=""):
     finally:
         for kk, _ in opts:
             D.set_option(kk, {"ws_mt": 0, "ws_epi_groups": 1, "splits": 0, "pair": 1, "pair_min_kb": 8,
-                              "pair_bn": 256, "shifted_window": 1, "tma_store": 0, "tail_split": 0, "stem_fused": 0,
+                              "pair_bn": 256, "pair_min_round": 1, "shifted_window": 1, "tma_store": 0, "tail_split": 0, "stem_fused": 0,
                               "splitk_inkernel": 1, "b_res": 0, "producers": 2, "s2d_one": 1}[kk])  # library defaults
     ran = D.last_launch()
     print(f"{label:34s} plan a_mode={plan['a_mode']} bm={plan['bm']} bn={plan['bn']} splits={plan['splits']} "
@@ -64,11 +64,11 @@ def main():
                label="fused stem odd extent requant")
     ok &= conv(2, 10, 256, 128, 3, 1, opts=[("splits", 3), ("splitk_inkernel", 0)], label="split-K + fix-up kernel")
     ok &= conv(2, 10, 256, 128, 3, 1, opts=[("splits", 3)], label="split-K, in-kernel fix-up")
-    ok &= conv(2, 10, 256, 256, 3, 1, opts=[("shifted_window", 0), ("pair", 1), ("pair_min_kb", 1)],
+    ok &= conv(2, 10, 256, 256, 3, 1, opts=[("shifted_window", 0), ("pair", 1), ("pair_min_kb", 1), ("pair_min_round", 0)],
                seed=False, scale=2.0 ** -13, label="conv_tc2 CTA pair")
     ok &= conv(2, 10, 64, 256, 1, 1, opts=[("shifted_window", 0), ("tma_store", 1)], seed=False,
                scale=2.0 ** -12, label="conv_tc TMA-store epilogue")
-    ok &= conv(3, 10, 128, 128, 3, 1, opts=[("shifted_window", 0), ("pair", 1), ("pair_min_kb", 1), ("pair_bn", 0)],
+    ok &= conv(3, 10, 128, 128, 3, 1, opts=[("shifted_window", 0), ("pair", 1), ("pair_min_kb", 1), ("pair_bn", 0), ("pair_min_round", 0)],
                seed=False, scale=2.0 ** -13, label="conv_tc2 CTA pair BN128")
     ok &= conv(4, 100, 128, 128, 3, 1, opts=[("shifted_window", 0), ("b_res", 1)], seed=False, scale=2.0 ** -13,
                label="conv_tc resident B (301 tiles)")
