@@ -52,7 +52,11 @@ struct Options {
   int tail_split = 0;           // split the under-filled last round of tiles along K
   int split_min_kb = 0;         // automatic split-K keeps >= this many K blocks per split (0: off)
   int splitk_inkernel = 1;      // split-K partials combined inside the kernel (last-arriver fix-up)
-  int pingpong_kb = 2;          // general kernel: ping-pong epilogue groups up to this many K blocks
+  // general kernel: ping-pong epilogue groups (2 x 8 warps on alternate
+  // accumulators) for tiles of up to this many K blocks.  Off by default since
+  // the requant fast path: one 16-warp group is faster on every thin-K layer
+  // (c3_1x1_128_512 34.8 -> 31.9 us) and the suite +1.1-1.3 % on one box.
+  int pingpong_kb = 0;
   int ws_mt = 0;                // shifted window: force 1/2/4 tiles per work unit (0 = automatic)
   int ws_1x1_k = 64;            // shifted window for 1x1 convs with K <= this many bytes
   int ws_1x1 = 0;               // ... for every 1x1 stride-1 conv

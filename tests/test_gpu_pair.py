@@ -13,7 +13,7 @@ from tests.gpu_helpers import to_dev
 pytestmark = pytest.mark.gpu
 # the library defaults (tzc_b200_internal.hpp Options): pairs for BN = 256
 # layers with >= 8 K blocks whose pair tiles fill a round of SM pairs
-DEFAULTS = {"pair": 1, "pair_min_kb": 8, "pair_bn": 256, "pair_min_round": 1, "tma_store": 0, "pingpong_kb": 2}
+DEFAULTS = {"pair": 1, "pair_min_kb": 8, "pair_bn": 256, "pair_min_round": 1, "tma_store": 0, "pingpong_kb": 0}
 FORCE = {"pair_min_kb": 1, "pair_bn": 0, "pair_min_round": 0, "pingpong_kb": 0}  # (pairs need one epilogue group)
 
 

@@ -117,7 +117,7 @@ def test_split_f16(cuda):
 
 
 @pytest.mark.parametrize("opts,n,hp", [({"b_res": 1}, 4, 100), ({"producers": 1}, 2, 20),
-                                       ({"b_res": 1, "producers": 1}, 4, 100)])
+                                       ({"b_res": 1, "producers": 1}, 4, 100), ({"pingpong_kb": 16}, 3, 20)])
 def test_general_kernel_pipeline_options(cuda, opts, n, hp):
     """The general kernel's operand-pipeline variants (resident B tile loaded
     once per CTA; one or two TMA producer warps) plan the same tiles and stay
@@ -138,6 +138,7 @@ def test_general_kernel_pipeline_options(cuda, opts, n, hp):
         D.set_option("shifted_window", 1)
         D.set_option("b_res", 0)
         D.set_option("producers", 2)
+        D.set_option("pingpong_kb", 0)
     ref = Orc.conv2d_nhwc(x, w, 1)
     assert np.array_equal(got, ref)
     assert np.array_equal(q, Orc.requant_i8(ref, 2.0 ** -13))

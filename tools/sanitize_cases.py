@@ -40,7 +40,7 @@ def conv(n, hp, c, k, r, st, opts=(), seed=True, scale=None, label=""):
         for kk, _ in opts:
             D.set_option(kk, {"ws_mt": 0, "ws_epi_groups": 1, "splits": 0, "pair": 1, "pair_min_kb": 8,
                               "pair_bn": 256, "pair_min_round": 1, "shifted_window": 1, "tma_store": 0, "tail_split": 0, "stem_fused": 0,
-                              "splitk_inkernel": 1, "b_res": 0, "producers": 2, "s2d_one": 1}[kk])  # library defaults
+                              "splitk_inkernel": 1, "b_res": 0, "producers": 2, "s2d_one": 1, "pingpong_kb": 0}[kk])  # library defaults
     ran = D.last_launch()
     print(f"{label:34s} plan a_mode={plan['a_mode']} bm={plan['bm']} bn={plan['bn']} splits={plan['splits']} "
           f"ran {ran['kernel']} cta_group={ran['cta_group']} bm={ran['bm']} bn={ran['bn']} "
@@ -73,6 +73,8 @@ def main():
     ok &= conv(4, 100, 128, 128, 3, 1, opts=[("shifted_window", 0), ("b_res", 1)], seed=False, scale=2.0 ** -13,
                label="conv_tc resident B (301 tiles)")
     ok &= conv(2, 10, 64, 128, 3, 1, opts=[("shifted_window", 0), ("producers", 1)], label="conv_tc one producer")
+    ok &= conv(2, 10, 64, 256, 1, 1, opts=[("shifted_window", 0), ("pingpong_kb", 16)], seed=False,
+               scale=2.0 ** -12, label="conv_tc ping-pong epilogue groups")
     ok &= conv(2, 62, 3, 64, 7, 2, opts=[("s2d_one", 0)], seed=False, scale=2.0 ** -11,
                label="s2d stem two-launch S2D")
     # fp16
