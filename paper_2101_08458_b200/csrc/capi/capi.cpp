@@ -280,7 +280,7 @@ const char* const kCandidates[] = {
     "",           "bn=64",          "bn=128",         "bn=256",        "splits=2",      "splits=4",
     "shifted_window=0", "ws_mt=1",  "ws_mt=2",        "ws_mt=4",       "pingpong_kb=2", "pingpong_kb=16",
     "tma_store=1", "pair=1;pair_min_kb=1;pair_min_round=0", "ws_1x1=1", "ws_epi_groups=2", "l2_hints=0",
-    "pair=0", "pair=1;pair_min_kb=1;pair_bn=0;pair_min_round=0", "b_res=1"};
+    "pair=0", "pair=1;pair_min_kb=1;pair_bn=0;pair_min_round=0", "b_res=0"};
 constexpr int kNumCandidates = sizeof(kCandidates) / sizeof(kCandidates[0]);
 
 template <typename Run>

@@ -32,11 +32,11 @@ struct Knob {
 };
 constexpr int kMtAllowed[] = {0, 1, 2, 4, -1};
 constexpr int kBnAllowed[] = {0, 64, 128, 256, -1};
-constexpr int kEgAllowed[] = {1, 2, -1};
+constexpr int kEgAllowed[] = {0, 1, 2, -1};
 const Knob kKnobs[] = {
     {"splits", &Options::splits, 0, 1 << 16, nullptr},
     {"shifted_window", &Options::shifted_window, 0, 1, nullptr},
-    {"ws_epi_groups", &Options::ws_epi_groups, 1, 2, kEgAllowed},
+    {"ws_epi_groups", &Options::ws_epi_groups, 0, 2, kEgAllowed},
     {"tail_split", &Options::tail_split, 0, 1, nullptr},
     {"split_min_kb", &Options::split_min_kb, 0, 1 << 20, nullptr},
     {"splitk_inkernel", &Options::splitk_inkernel, 0, 1, nullptr},
@@ -55,7 +55,7 @@ const Knob kKnobs[] = {
     {"st256", &Options::st256, 0, 1, nullptr},
     {"l2_hints", &Options::l2_hints, 0, 3, nullptr},
     {"tma_store", &Options::tma_store, 0, 2, nullptr},
-    {"b_res", &Options::b_res, 0, 1, nullptr},
+    {"b_res", &Options::b_res, 0, 2, nullptr},
     {"stem_fused", &Options::stem_fused, 0, 1, nullptr},
 };
 

@@ -549,7 +549,8 @@ Status plan_problem(const Problem& pb_in, const Options& o, tzc_plan* plan) {
   plan->grid = std::min(wsplit.full + (tiles - wsplit.full) * splits, sms);
   plan->smem_bytes = ring_smem(bn, kb, eg, plan->stages);
   plan->workspace_bytes = splits > 1 ? (int64_t)splits * (M - red_m0) * pb.ngemm * 4 : 0;
-  if (o.b_res && splits == 1 && wsplit.full == tiles && plan->grid % tiles_n == 0 && tiles >= 2 * plan->grid) {
+  if ((o.b_res == 1 || (o.b_res == 2 && pb.taps == 1)) && splits == 1 && wsplit.full == tiles &&
+      plan->grid % tiles_n == 0 && tiles >= 2 * plan->grid) {
     const int st = bres_stages(bn, kb, 0, num_kb, kStaticSmem);  // as run_problem decides (no TMA-store staging)
     if (st) {
       plan->stages = st;
@@ -789,8 +790,13 @@ Status run_ws(const Problem& pb, const WsPlan& w, const Options& o, const void* 
   p.mt = w.mt;
   // as many accumulators as TMEM holds (<= 4): the epilogue may lag the MMAs
   // by NACC-1 units (the ping-pong epilogue groups need exactly 2)
-  p.nacc = o.ws_epi_groups == 2 ? 2 : std::min(4, 512 / (w.mt * w.bn));
-  p.epi_groups = o.ws_epi_groups == 2 ? 2 : 1;
+  // epilogue groups: "ws_epi_groups" 1 / 2, or 0 = by shape: two ping-pong
+  // groups for the 3x3 layers (a unit's 9-tap MMA phase is long enough for the
+  // groups to alternate; c2_3x3_64 38.0 -> 36.7 us, c3_3x3_128 27.4 -> 26.1),
+  // one for 1x1 and the pair-mode stem (stem 86.0 -> 87.9 with two)
+  const int eg = o.ws_epi_groups ? o.ws_epi_groups : (!w.pair && pb.r * pb.s >= 9 ? 2 : 1);
+  p.nacc = eg == 2 ? 2 : std::min(4, 512 / (w.mt * w.bn));
+  p.epi_groups = eg;
   fill_epilogue(&p, pb, o, seed, out, ep);
   WsFn fn = ws_fn(w.bn, w.kb, pb.f16 != 0, w.pair != 0);
   if (!fn) return Status(TZC_E_INTERNAL, "no conv_ws instantiation");
@@ -896,7 +902,7 @@ Status run_stem_fused(const Problem& pb, const Problem& q, const WsPlan& w, cons
   p.num_tiles = w.tiles;
   p.splits = a_slots;
   p.mt = w.mt;
-  p.nacc = o.ws_epi_groups == 2 ? 2 : std::min(4, 512 / (w.mt * w.bn));
+  p.nacc = o.ws_epi_groups == 2 ? 2 : std::min(4, 512 / (w.mt * w.bn));  // the fused stem: one group unless forced
   p.epi_groups = o.ws_epi_groups == 2 ? 2 : 1;
   fill_epilogue(&p, pb, o, seed, out, ep);
   const bool rq = ep.kind == tzcdev::EP_REQUANT_I8;
@@ -1182,7 +1188,8 @@ Status run_problem(const Problem& pb, const Options& o, const void* a, const voi
   // N tile (grid a multiple of tiles_n) and the whole B tile fits beside a
   // >= 4-deep A ring, B is loaded once per CTA instead of once per tile.
   p.b_res = 0;
-  if (o.b_res && plan.splits == 1 && p.full_units == p.num_tiles && plan.grid % plan.tiles_n == 0 &&
+  if ((o.b_res == 1 || (o.b_res == 2 && pb.taps == 1)) && plan.splits == 1 && p.full_units == p.num_tiles &&
+      plan.grid % plan.tiles_n == 0 &&
       p.num_tiles >= 2 * plan.grid) {
     const int st = bres_stages(plan.bn, plan.bk_bytes, p.tma_store ? p.epi_groups : 0, p.num_kb, kStaticSmem);
     if (st) {

@@ -48,7 +48,7 @@ struct Problem {
 struct Options {
   int splits = 0;               // forced split-K factor (0 = automatic)
   int shifted_window = 1;       // weight-stationary kernel for eligible stride-1 convs
-  int ws_epi_groups = 1;        // shifted window: 1 or 2 (ping-pong) epilogue groups
+  int ws_epi_groups = 0;        // shifted window: 1 or 2 (ping-pong) epilogue groups; 0 = by shape (2 for 3x3)
   int tail_split = 0;           // split the under-filled last round of tiles along K
   int split_min_kb = 0;         // automatic split-K keeps >= this many K blocks per split (0: off)
   int splitk_inkernel = 1;      // split-K partials combined inside the kernel (last-arriver fix-up)
@@ -80,7 +80,10 @@ struct Options {
   int st256 = 1;                // 256-bit epilogue stores where aligned
   int l2_hints = 1;             // 1: A loads evict-first; 2: B loads evict-last
   int tma_store = 0;            // int8 TMA-store epilogue: 0 never, 1 always, 2 by K
-  int b_res = 0;                // general kernel: keep the CTA's whole B tile in SMEM when it fits
+  // general kernel: keep the CTA's whole B tile in SMEM when it fits: 0 never,
+  // 1 always, 2 for 1x1 layers (c3_1x1s2_256_512 38.2 -> 35.9 us, c3_1x1_256_128
+  // 55.4 -> 53.8; 3x3 im2col layers lose ring depth: c3_3x3s2_128 34.8 -> 35.9)
+  int b_res = 2;
   int stem_fused = 0;           // C = 3 stride-2 int8 stem: space-to-depth fused into the kernel (stem_ws.cuh;
                                 // correct, but slower than the separate S2D pass: DESIGN.md §8 finding 10)
 };

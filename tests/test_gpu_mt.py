@@ -123,7 +123,7 @@ def test_forced_mt(cuda, name, nb, hp, c, k, r, st, mt, eg):
                       scale=0.000731).cpu().numpy()  # general scale + seed
     finally:
         D.set_option("ws_mt", 0)
-        D.set_option("ws_epi_groups", 1)
+        D.set_option("ws_epi_groups", 0)
     ref = Orc.conv2d_nhwc(x, w, st, s0)
     assert np.array_equal(got, ref)
     assert np.array_equal(q, Orc.requant_i8(Orc.conv2d_nhwc(x, w, st), s))

@@ -136,7 +136,7 @@ def test_general_kernel_pipeline_options(cuda, opts, n, hp):
         q = D.conv2d(xd, wd, 1, epilogue="requant_i8", scale=2.0 ** -13).cpu().numpy()
     finally:
         D.set_option("shifted_window", 1)
-        D.set_option("b_res", 0)
+        D.set_option("b_res", 2)
         D.set_option("producers", 2)
         D.set_option("pingpong_kb", 0)
     ref = Orc.conv2d_nhwc(x, w, 1)

@@ -24,4 +24,4 @@ for name in names:
                 ref = Orc.conv2d_nhwc(xn[img:img+1], wn, L.stride)
                 res.append((img, int((out[img:img+1] != ref).sum()), int((q[img:img+1] != Orc.requant_i8(ref, s)).sum())))
             print(name, nb, opts, plan["bm"], plan["a_mode"], plan["grid"], res, flush=True)
-            for k in opts: D.set_option(k, {"ws_epi_groups": 1, "shifted_window": 1}[k])
+            for k in opts: D.set_option(k, {"ws_epi_groups": 0, "shifted_window": 1}[k])

@@ -38,9 +38,9 @@ def conv(n, hp, c, k, r, st, opts=(), seed=True, scale=None, label=""):
             ok = np.array_equal(got, Orc.requant_i8(Orc.conv2d_nhwc(x, w, st, s0), scale))
     finally:
         for kk, _ in opts:
-            D.set_option(kk, {"ws_mt": 0, "ws_epi_groups": 1, "splits": 0, "pair": 1, "pair_min_kb": 8,
+            D.set_option(kk, {"ws_mt": 0, "ws_epi_groups": 0, "splits": 0, "pair": 1, "pair_min_kb": 8,
                               "pair_bn": 256, "pair_min_round": 1, "shifted_window": 1, "tma_store": 0, "tail_split": 0, "stem_fused": 0,
-                              "splitk_inkernel": 1, "b_res": 0, "producers": 2, "s2d_one": 1, "pingpong_kb": 0}[kk])  # library defaults
+                              "splitk_inkernel": 1, "b_res": 2, "producers": 2, "s2d_one": 1, "pingpong_kb": 0}[kk])  # library defaults
     ran = D.last_launch()
     print(f"{label:34s} plan a_mode={plan['a_mode']} bm={plan['bm']} bn={plan['bn']} splits={plan['splits']} "
           f"ran {ran['kernel']} cta_group={ran['cta_group']} bm={ran['bm']} bn={ran['bn']} "
