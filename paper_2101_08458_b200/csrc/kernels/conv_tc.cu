@@ -31,8 +31,8 @@ int g_debug_flags = 0;  // tools/trace_ws only
 #endif
 
 namespace {
-#ifdef TZC_TRACE
-constexpr int kStaticSmem = 1024;  // s_trace
+#if defined(TZC_TRACE) || defined(TZC_CHECKS)
+constexpr int kStaticSmem = 1024;  // s_trace / the checks build's per-CTA store bounds
 #else
 constexpr int kStaticSmem = 0;
 #endif
@@ -219,22 +219,10 @@ namespace {
 // prologue (barrier init, TMEM alloc, descriptor prefetch) overlaps the
 // previous grid's tail; griddepcontrol.wait in the kernel keeps the data
 // dependency.  Captured into CUDA graphs as programmatic edges.
-#ifdef TZC_CHECKS
-// Instrumented build: the launch's legal store ranges (single-stream validation runs only).
-void set_check_bounds(const ConvKernelParams& p, cudaStream_t stream) {
-  unsigned long long lo[2] = {reinterpret_cast<unsigned long long>(p.out), reinterpret_cast<unsigned long long>(p.partial)};
-  unsigned long long hi[2] = {lo[0] + (unsigned long long)p.out_bytes, lo[1] + (unsigned long long)p.partial_bytes};
-  cudaMemcpyToSymbolAsync(tzcdev::g_chk_lo, lo, sizeof(lo), 0, cudaMemcpyHostToDevice, stream);
-  cudaMemcpyToSymbolAsync(tzcdev::g_chk_hi, hi, sizeof(hi), 0, cudaMemcpyHostToDevice, stream);
-}
-#endif
 
 template <typename Kern>
 cudaError_t launch_pdl(Kern kern, dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
                        const ConvKernelParams& p) {
-#ifdef TZC_CHECKS
-  set_check_bounds(p, stream);
-#endif
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = block;
@@ -288,9 +276,6 @@ Status launch_pair(const ConvKernelParams& p, int grid, cudaStream_t stream) {
   attr[1].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 2;
-#ifdef TZC_CHECKS
-  set_check_bounds(p, stream);
-#endif
   cudaError_t e = cudaLaunchKernelEx(&cfg, kern, p);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   note_launch(3, 2, 256, BN, 128, AM, grid, 1);

@@ -218,12 +218,23 @@ __device__ __forceinline__ uint32_t requant_general(int32_t c, float s) {
 
 #ifdef TZC_CHECKS
 // Instrumented build: every epilogue store lies inside [out, out + out_bytes)
-// or [partial, partial + partial_bytes) (host-computed extents).
-__device__ unsigned long long g_chk_lo[2], g_chk_hi[2];
+// or [partial, partial + partial_bytes) (host-computed extents, carried in the
+// launch's own parameters and copied to per-CTA shared memory at kernel start,
+// so concurrent launches and CUDA-graph replays each check their own ranges).
+__shared__ unsigned long long s_chk_lo[2], s_chk_hi[2];
+__device__ __forceinline__ void chk_init(const ConvKernelParams& p) {
+  if (threadIdx.x == 0) {
+    s_chk_lo[0] = reinterpret_cast<unsigned long long>(p.out);
+    s_chk_hi[0] = s_chk_lo[0] + (unsigned long long)p.out_bytes;
+    s_chk_lo[1] = reinterpret_cast<unsigned long long>(p.partial);
+    s_chk_hi[1] = s_chk_lo[1] + (unsigned long long)p.partial_bytes;
+  }
+  __syncthreads();
+}
 __device__ __forceinline__ void chk_store(const void* ptr, int bytes) {
   const unsigned long long a = reinterpret_cast<unsigned long long>(ptr);
   bool ok = false;
-  for (int r = 0; r < 2; ++r) ok = ok || (a >= g_chk_lo[r] && a + bytes <= g_chk_hi[r]);
+  for (int r = 0; r < 2; ++r) ok = ok || (a >= s_chk_lo[r] && a + bytes <= s_chk_hi[r]);
   if (!ok) {
     printf("tzc bounds: block %d thread %d stores %d bytes at %p outside the output / workspace\n", blockIdx.x,
            threadIdx.x, bytes, ptr);
@@ -231,9 +242,13 @@ __device__ __forceinline__ void chk_store(const void* ptr, int bytes) {
   }
 }
 #define TZC_CHK_STORE(p, n) chk_store((p), (n))
+#define TZC_CHK_INIT(p) chk_init(p)
 #else
 #define TZC_CHK_STORE(p, n) \
   do {                      \
+  } while (0)
+#define TZC_CHK_INIT(p) \
+  do {                  \
   } while (0)
 #endif
 
@@ -602,6 +617,7 @@ __global__ void __launch_bounds__(EpiCfg<BN>::THREADS, 1) conv_tc_kernel(const _
   extern __shared__ uint8_t smem_raw[];
   TZC_TRACE_DECL
   TZC_TRACE_INIT;
+  TZC_CHK_INIT(p);
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sStage = smem;  // TMA-store staging: EG tiles of STAGING_BYTES (1024-aligned)
   uint8_t* sA = smem + (p.tma_store ? EG * Cfg::STAGING_BYTES : 0);
@@ -958,6 +974,7 @@ __global__ void __launch_bounds__(EpiCfg<BN>::THREADS, 1) conv_tc_kernel(const _
 // combined in split order.
 template <bool kF16, int kEpm>
 __global__ void splitk_reduce_kernel(const __grid_constant__ ConvKernelParams p) {
+  TZC_CHK_INIT(p);
   pdl_launch_dependents();
   pdl_wait();
   const int64_t groups = (int64_t)p.red_rows * (p.Ngemm / 16);

@@ -43,6 +43,7 @@ __global__ void __launch_bounds__(EpiCfg<BN>::THREADS, 1) conv_tc2_kernel(const 
   const int STAGES = p.stages;
 
   extern __shared__ uint8_t smem_raw[];
+  TZC_CHK_INIT(p);
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sStage = smem;
   uint8_t* sA = smem + Cfg::STAGING_BYTES;

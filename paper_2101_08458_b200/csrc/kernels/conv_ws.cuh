@@ -55,6 +55,7 @@ __global__ void __launch_bounds__(EpiCfg<BN>::THREADS, 1) conv_ws_kernel(const _
   extern __shared__ uint8_t smem_raw[];
   TZC_TRACE_DECL
   TZC_TRACE_INIT;
+  TZC_CHK_INIT(p);
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sB = smem;
   uint8_t* sA = smem + ((b_bytes + 1023) / 1024) * 1024;
