@@ -50,6 +50,7 @@ const Knob kKnobs[] = {
     {"pair_bn", &Options::pair_bn, 0, 256, nullptr},
     {"pair_min_round", &Options::pair_min_round, 0, 64, nullptr},
     {"s2d_one", &Options::s2d_one, 0, 1, nullptr},
+    {"l2_a_max_out_mb", &Options::l2_a_max_out_mb, 0, 1 << 20, nullptr},
     {"producers", &Options::producers, 1, 2, nullptr},
     {"pair", &Options::pair, 0, 1, nullptr},
     {"st256", &Options::st256, 0, 1, nullptr},

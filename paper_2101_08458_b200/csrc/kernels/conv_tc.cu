@@ -1114,6 +1114,12 @@ Status run_problem(const Problem& pb, const Options& o, const void* a, const voi
   p.fd_cblocks = make_fdiv(std::max(1, p.c_blocks));
   p.fd_s = make_fdiv(std::max(1, pb.s));
   fill_epilogue(&p, pb, o, seed, out, ep);
+  // A evict-first only while the output fits L2 beside the streams: then the
+  // output stays resident and the read-once activations make room for it
+  // (c2_1x1_256_64 38.4 vs 45.1 us without the hint); a larger output is
+  // written back during the kernel anyway and the hint only hurts
+  // (c3_1x1_256_128, 103 MB out: 55.4 vs 49.3 us).  Sweep: profiles/r02c_sweep*.md
+  if (o.l2_a_max_out_mb > 0 && p.out_bytes > ((int64_t)o.l2_a_max_out_mb << 20)) p.pol_a = 0;
   if (ep.kind == tzcdev::EP_REQUANT_I8 && p.full_units > 0 && p.vec_ok && pb.out.nb == pb.ngemm &&
       pb.out.stride_m == pb.ngemm && pb.ngemm % plan.bn == 0 &&
       (o.tma_store == 1 || (o.tma_store == 2 && (int64_t)p.num_kb * plan.bk_bytes <= o.tma_store_k))) {

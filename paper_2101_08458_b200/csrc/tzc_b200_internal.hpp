@@ -75,6 +75,7 @@ struct Options {
   // fewer (batch 32) a cluster's two-SM footprint backfills the SMs other graph
   // branches leave idle worse (batch 32: 682-690 TOPS without pairs, 655-677 with)
   int pair_min_round = 1;
+  int l2_a_max_out_mb = 64;     // general kernel: A evict-first hint only for outputs <= this many MB (0: always)
   int s2d_one = 1;              // int8 C=3 stem: S2D rows + weight rearrangement in one launch
   int producers = 2;            // TMA producer warps of the general / pair kernels (1 or 2)
   int st256 = 1;                // 256-bit epilogue stores where aligned
