@@ -162,7 +162,7 @@ def test_tuner_installs_a_plan_and_results_stay_exact(cuda):
         best, log = D.tune_conv2d(x, w, 1, epilogue="requant_i8", scale=2.0 ** -12, reps=3)
         lines = log.strip().splitlines()
         assert sum(ln.startswith("candidate ") for ln in lines) == 20 and lines[-1].startswith(f"best {best} ")
-        assert 0 <= best < 17
+        assert 0 <= best < len(D.tune_candidates())
         q = D.conv2d(x, w, 1, epilogue="requant_i8", scale=2.0 ** -12).cpu().numpy()
         assert np.array_equal(q, Orc.requant_i8(ref, 2.0 ** -12))
         a = torch.from_numpy(Orc.random_tensor("u8", (384, 256), 5)).to(dev)
